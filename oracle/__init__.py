@@ -1,0 +1,188 @@
+"""tcx ORACLE — plain, slow, obviously-correct CPU implementation of the hot path.
+
+TEST INFRASTRUCTURE.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The product package
+(``paper_2206_02874_b200``) never imports it, and the two share no code: the C sources
+here (``tcxref.c``, ``models.c``) are compiled into their own ``libtcxref.so``.
+
+Definitions (cited in the C sources):
+  * ``D = A x B + C`` (§II-A); "row.col": A is m x k row-major, B is stored
+    n x k.
+  * FP16/BF16/TF32 -> FP32: every product exact, the sum exact, ONE RNE rounding to FP32.
+  * INT8 -> INT32: exact int64 sum, two's-complement wrap to 32 bits.
+  * 2:4 sparse: expand(sA, meta) then dense.
+
+Every function is pinned by ``tests/test_oracle_*.py`` against brute-force rational
+arithmetic, closed forms, SPEC worked examples and the paper's zero-error cells.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libtcxref.so")
+_SRCS = [os.path.join(_HERE, "tcxref.c"), os.path.join(_HERE, "models.c")]
+
+# format ids (oracle-local; deliberately not imported from the product header)
+F16, BF16, TF32, F32, S8, S32 = 0, 1, 2, 3, 4, 5
+_NP = {F16: np.uint16, BF16: np.uint16, TF32: np.uint32, F32: np.uint32, S8: np.int8, S32: np.int32}
+
+
+def build(force: bool = False) -> str:
+    """Compile libtcxref.so with gcc (-O2, no fast-math, no FMA contraction)."""
+    newest = max(os.path.getmtime(s) for s in _SRCS)
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < newest:
+        cmd = ["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-ffp-contract=off",
+               "-fno-fast-math", "-pthread", "-o", _LIB_PATH] + _SRCS + ["-lm"]
+        subprocess.check_call(cmd)
+    return _LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB_PATH)
+        vp, i64, u32, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_int, ctypes.c_double
+        L.tcxref_quantize.argtypes = [dbl, i32, i32]; L.tcxref_quantize.restype = u32
+        L.tcxref_decode.argtypes = [i32, u32]; L.tcxref_decode.restype = dbl
+        L.tcxref_dot_fp.argtypes = [i32, i64, vp, vp, u32, ctypes.POINTER(dbl)]; L.tcxref_dot_fp.restype = u32
+        L.tcxref_dot_s8.argtypes = [i64, vp, vp, ctypes.c_int32]; L.tcxref_dot_s8.restype = ctypes.c_int32
+        L.tcxref_sum_round.argtypes = [i32, vp, vp, vp, i32, i32]; L.tcxref_sum_round.restype = u32
+        L.tcxref_gemm_samples.argtypes = [i32, i64, vp, i64, vp, i64, vp, i64, i64, vp, vp, vp, vp, i32]
+        L.tcxref_gemm_samples.restype = i32
+        L.tcxref_sp24_expand.argtypes = [i32, i64, i64, vp, i64, vp, vp, i64]; L.tcxref_sp24_expand.restype = i64
+        L.tcxref_sp24_compress.argtypes = [i32, i64, i64, vp, i64, vp, i64, vp]; L.tcxref_sp24_compress.restype = i64
+        L.tcxref_tiles.argtypes = [i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]; L.tcxref_tiles.restype = i32
+        L.tcxref_model_dot.argtypes = [i32, i32, vp, vp, u32, i32, i32, i32, i32, i32, i32]
+        L.tcxref_model_dot.restype = u32
+        L.tcxref_seq32.argtypes = [i32, vp, vp, ctypes.c_float, i32]; L.tcxref_seq32.restype = ctypes.c_float
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None else None
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+# ---------------------------------------------------------------------------- formats
+def quantize(x: float, fmt: int, rz: bool = False) -> int:
+    """SPEC.md:38-46 quantize(x, fmt, NearestEven|TowardZero) -> stored bits."""
+    return int(lib().tcxref_quantize(float(x), fmt, int(rz)))
+
+
+def decode(fmt: int, bits: int) -> float:
+    return float(lib().tcxref_decode(fmt, int(bits) & 0xFFFFFFFF))
+
+
+def quantize_array(x: np.ndarray, fmt: int) -> np.ndarray:
+    L = lib()
+    flat = np.asarray(x, dtype=np.float64).ravel()
+    out = np.fromiter((L.tcxref_quantize(float(v), fmt, 0) for v in flat), dtype=np.uint32, count=flat.size)
+    return out.astype(_NP[fmt]).reshape(np.shape(x))
+
+
+# ---------------------------------------------------------------------------- dots
+def dot_fp(ab: int, a_bits: np.ndarray, b_bits: np.ndarray, c_bits: int = 0):
+    """One FP output element: RNE_fp32(c + sum a_k b_k) exactly; returns (bits, sum|ab|+|c|)."""
+    a = _c(a_bits, _NP[ab]); b = _c(b_bits, _NP[ab])
+    absv = ctypes.c_double(0.0)
+    r = lib().tcxref_dot_fp(ab, a.size, _p(a), _p(b), int(c_bits) & 0xFFFFFFFF, ctypes.byref(absv))
+    return int(r), absv.value
+
+
+def dot_s8(a: np.ndarray, b: np.ndarray, c: int = 0) -> int:
+    a = _c(a, np.int8); b = _c(b, np.int8)
+    return int(lib().tcxref_dot_s8(a.size, _p(a), _p(b), int(c)))
+
+
+def sum_round(signs, mants, exps, out_fmt=F32, rz=False) -> int:
+    s = _c(signs, np.int32); m = _c(mants, np.uint64); e = _c(exps, np.int32)
+    return int(lib().tcxref_sum_round(len(s), _p(s), _p(m), _p(e), out_fmt, int(rz)))
+
+
+def gemm_samples(ab: int, A: np.ndarray, B: np.ndarray, C, rows, cols, nthreads: int | None = None):
+    """D[rows[s], cols[s]] for A (M x K), B (N x K, 'col'), C (M x N or None).
+
+    Returns (out, abs) where out is uint32 bits (FP32 bits, or int32 bits for S8) and abs is
+    the float64 bound magnitude sum_k|a b| + |c| (FP only)."""
+    A = np.ascontiguousarray(A); B = np.ascontiguousarray(B)
+    assert A.dtype == _NP[ab] and B.dtype == _NP[ab], (A.dtype, B.dtype)
+    M, K = A.shape
+    N, K2 = B.shape
+    assert K == K2
+    rows = _c(rows, np.int64); cols = _c(cols, np.int64)
+    n = rows.size
+    out = np.zeros(n, dtype=np.uint32)
+    absv = np.zeros(n, dtype=np.float64)
+    Cc = None
+    if C is not None:
+        Cc = np.ascontiguousarray(C)
+        assert Cc.shape == (M, N) and Cc.itemsize == 4
+    nt = nthreads or len(os.sched_getaffinity(0))
+    rc = lib().tcxref_gemm_samples(ab, K, _p(A), K, _p(B), K, _p(Cc) if Cc is not None else None,
+                                   N, n, _p(rows), _p(cols), _p(out), _p(absv), nt)
+    assert rc == 0
+    return out, absv
+
+
+def gemm_full(ab: int, A, B, C=None, nthreads=None):
+    M = A.shape[0]; N = B.shape[0]
+    ii, jj = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+    out, absv = gemm_samples(ab, A, B, C, ii.ravel(), jj.ravel(), nthreads)
+    return out.reshape(M, N), absv.reshape(M, N)
+
+
+def tiles(ab: int, m: int, n: int, k: int, A, B, C):
+    """Batch of independent tiles: D_t = A_t B_t + C_t (layouts as tcx_mma_tiles)."""
+    A = np.ascontiguousarray(A); B = np.ascontiguousarray(B)
+    count = A.size // (m * k)
+    Cc = np.ascontiguousarray(C) if C is not None else None
+    D = np.zeros(count * m * n, dtype=np.uint32)
+    absv = np.zeros(count * m * n, dtype=np.float64)
+    lib().tcxref_tiles(ab, m, n, k, count, _p(A), _p(B), _p(Cc) if Cc is not None else None, _p(D), _p(absv))
+    return D.reshape(count, m, n), absv.reshape(count, m, n)
+
+
+# ---------------------------------------------------------------------------- 2:4 sparse
+def sp24_expand(vals: np.ndarray, meta: np.ndarray, K: int) -> np.ndarray:
+    vals = np.ascontiguousarray(vals); meta = _c(meta, np.uint32)
+    M = vals.shape[0]
+    dense = np.zeros((M, K), dtype=vals.dtype)
+    bad = lib().tcxref_sp24_expand(vals.itemsize, M, K, _p(vals), vals.shape[1], _p(meta), _p(dense), K)
+    if bad >= 0:
+        raise ValueError(f"bad metadata nibble at row {bad // (K // 4)}, group {bad % (K // 4)}")
+    return dense
+
+
+def sp24_compress(dense: np.ndarray):
+    dense = np.ascontiguousarray(dense)
+    M, K = dense.shape
+    vals = np.zeros((M, K // 2), dtype=dense.dtype)
+    meta = np.zeros((M, K // 32), dtype=np.uint32)
+    bad = lib().tcxref_sp24_compress(dense.itemsize, M, K, _p(dense), K, _p(vals), K // 2, _p(meta))
+    return vals, meta, int(bad)
+
+
+# ---------------------------------------------------------------------------- probe models
+def model_dot(ab: int, a_bits, b_bits, c_bits: int, Ki: int, g: int, p: int, rz: bool,
+              floor_mode: bool = False, c_after: bool = False) -> int:
+    a = _c(a_bits, _NP[ab]); b = _c(b_bits, _NP[ab])
+    return int(lib().tcxref_model_dot(ab, a.size, _p(a), _p(b), int(c_bits) & 0xFFFFFFFF, Ki, g, p,
+                                      int(rz), int(floor_mode), int(c_after)))
+
+
+def seq32(a: np.ndarray, b: np.ndarray, c: float, c_last: bool = False) -> float:
+    a = _c(a, np.float32); b = _c(b, np.float32)
+    return float(lib().tcxref_seq32(a.size, _p(a), _p(b), float(c), int(c_last)))

@@ -1,0 +1,202 @@
+"""tcxgen — seeded synthetic input generators shared by tests, bench and the oracle checks.
+
+This module holds NONE of the method's arithmetic (no products, sums, MMA, 2:4 expansion):
+it only draws random numbers and rounds reals into the stated input formats.  Both the
+CUDA path (via device tensors) and the oracle (via host copies of the very same bytes)
+consume its output, so no input ever comes from the CUDA path.
+
+Generator (pinned; deterministic regardless of device or chunking):
+  * counter-based SplitMix64: z = seed*0x9E3779B97F4A7C15 + (stream << 48) + index, then the
+    standard SplitMix64 finaliser (precedent: SPEC.md:425-426 pins SplitMix64 + Box-Muller);
+  * uniform [0,1) = (z >> 11) * 2^-53;
+  * N(0,1) = Box-Muller cosine branch from draws 2i, 2i+1 (float64);
+  * reals are float64, rounded RNE to FP32 and then RNE to the target format
+    (FP16 / BF16 / TF32-in-FP32).  The paper uses N(0,1) with one shared seed
+    (PAPER.md:900); its generator is unpublished.
+  * int8 = top byte of z; int32 in [-2^20, 2^20] = (z >> 32) mod (2^21 + 1) - 2^20;
+    2:4 pair = (z >> 32) mod 6 over {(0,1),(0,2),(0,3),(1,2),(1,3),(2,3)}.
+Streams: A=1, B=2, C=3, positions=4, sparse values=5, probe classes=16+class.
+
+Works on CPU or CUDA torch tensors (torch is plumbing here, as in the product).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+GOLDEN = 0x9E3779B97F4A7C15
+M1 = 0xBF58476D1CE4E5B9
+M2 = 0x94D049BB133111EB
+STREAM_A, STREAM_B, STREAM_C, STREAM_POS, STREAM_SPVAL = 1, 2, 3, 4, 5
+PAIRS = ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))
+
+
+def _s64(x: int) -> int:
+    x &= (1 << 64) - 1
+    return x - (1 << 64) if x >= (1 << 63) else x
+
+
+def _srl(z: torch.Tensor, s: int) -> torch.Tensor:
+    """logical right shift of a uint64 held in int64"""
+    return (z >> s) & ((1 << (64 - s)) - 1)
+
+
+def splitmix_ref(seed: int, stream: int, index: int) -> int:
+    """pure-Python SplitMix64 (the definition the torch version is tested against)"""
+    m = (1 << 64) - 1
+    z = (seed * GOLDEN + (stream << 48) + index) & m
+    z = ((z ^ (z >> 30)) * M1) & m
+    z = ((z ^ (z >> 27)) * M2) & m
+    return z ^ (z >> 31)
+
+
+def splitmix(seed: int, stream: int, idx: torch.Tensor) -> torch.Tensor:
+    """uint64 words (as int64 bit patterns) for counters idx (int64 tensor)."""
+    base = _s64(seed * GOLDEN + (stream << 48))
+    z = idx + base
+    z = (z ^ _srl(z, 30)) * _s64(M1)
+    z = (z ^ _srl(z, 27)) * _s64(M2)
+    return z ^ _srl(z, 31)
+
+
+def _chunks(n: int, chunk: int = 1 << 24):
+    for s in range(0, n, chunk):
+        yield s, min(n, s + chunk)
+
+
+def uniform01(seed, stream, start, n, device="cpu") -> torch.Tensor:
+    idx = torch.arange(start, start + n, dtype=torch.int64, device=device)
+    z = splitmix(seed, stream, idx)
+    return _srl(z, 11).to(torch.float64) * (2.0 ** -53)
+
+
+def normal(seed, stream, start, n, device="cpu") -> torch.Tensor:
+    """N(0,1) in float64: Box-Muller cosine branch on draws (2i, 2i+1)."""
+    idx = torch.arange(2 * start, 2 * (start + n), dtype=torch.int64, device=device)
+    z = splitmix(seed, stream, idx)
+    u = _srl(z, 11).to(torch.float64) * (2.0 ** -53)
+    u1, u2 = u[0::2], u[1::2]
+    return torch.sqrt(-2.0 * torch.log1p(-u1)) * torch.cos((2.0 * math.pi) * u2)
+
+
+def round_tf32_bits(x32: torch.Tensor) -> torch.Tensor:
+    """FP32 -> TF32 round-to-nearest-even, stored in FP32 (low 13 bits zero).
+    NaN/inf untouched; a carry out of max-finite becomes inf."""
+    u = x32.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    expall = (u & 0x7F800000) == 0x7F800000
+    r = (u + 0xFFF + ((u >> 13) & 1)) & 0xFFFFE000
+    r = torch.where(expall, u, r)
+    r = torch.where(r >= (1 << 31), r - (1 << 32), r)
+    return r.to(torch.int32).view(torch.float32)
+
+
+def to_format(x64: torch.Tensor, fmt: str) -> torch.Tensor:
+    """float64 reals -> stored format: 'f16' | 'bf16' | 'tf32' (FP32 storage) | 'f32'."""
+    x32 = x64.to(torch.float32)
+    if fmt == "f32":
+        return x32
+    if fmt == "tf32":
+        return round_tf32_bits(x32)
+    if fmt == "f16":
+        return x32.to(torch.float16)
+    if fmt == "bf16":
+        return x32.to(torch.bfloat16)
+    raise ValueError(fmt)
+
+
+def _fill(out_flat: torch.Tensor, fn, chunk=1 << 24):
+    n = out_flat.numel()
+    for s, e in _chunks(n, chunk):
+        out_flat[s:e] = fn(s, e - s)
+    return out_flat
+
+
+def normal_matrix(shape, fmt, seed, stream, device="cpu", redraw_zero=False) -> torch.Tensor:
+    """matrix of N(0,1) rounded to fmt; element (i, j) uses counter i*cols + j.
+    redraw_zero: values that round to +-0 are replaced by a draw from stream+64 at the
+    same counter (repeated until nonzero) — the C5 "exactly 2 nonzeros" rule."""
+    n = int(math.prod(shape))
+    dt = {"f16": torch.float16, "bf16": torch.bfloat16, "tf32": torch.float32, "f32": torch.float32}[fmt]
+    out = torch.empty(n, dtype=dt, device=device)
+
+    def fn(s, m):
+        v = to_format(normal(seed, stream, s, m, device), fmt)
+        if redraw_zero:
+            k = 1
+            while True:
+                z = v == 0
+                if not bool(z.any()):
+                    break
+                alt = to_format(normal(seed, stream + 64 * k, s, m, device), fmt)
+                v = torch.where(z, alt, v)
+                k += 1
+        return v
+    _fill(out, fn)
+    return out.view(*shape)
+
+
+def uniform_matrix(shape, fmt, seed, stream, lo=-1.0, hi=1.0, device="cpu") -> torch.Tensor:
+    """reals uniform in [lo, hi) then RNE to fmt ([-1,1) then RNE; +-1 reachable)."""
+    n = int(math.prod(shape))
+    dt = {"f16": torch.float16, "bf16": torch.bfloat16, "tf32": torch.float32, "f32": torch.float32}[fmt]
+    out = torch.empty(n, dtype=dt, device=device)
+    _fill(out, lambda s, m: to_format(lo + (hi - lo) * uniform01(seed, stream, s, m, device), fmt))
+    return out.view(*shape)
+
+
+def int8_matrix(shape, seed, stream, device="cpu") -> torch.Tensor:
+    """uniform int8 in [-128, 127] (inclusive): top byte of z."""
+    n = int(math.prod(shape))
+    out = torch.empty(n, dtype=torch.int8, device=device)
+
+    def fn(s, m):
+        z = splitmix(seed, stream, torch.arange(s, s + m, dtype=torch.int64, device=device))
+        return (_srl(z, 56) - 128).to(torch.int8)   # top byte, re-centred (a bijection of the byte)
+    _fill(out, fn)
+    return out.view(*shape)
+
+
+def int32_matrix(shape, seed, stream, lo=-(1 << 20), hi=(1 << 20), device="cpu") -> torch.Tensor:
+    """uniform int32 in [lo, hi] inclusive: (z >> 32) mod (hi-lo+1) + lo."""
+    n = int(math.prod(shape))
+    out = torch.empty(n, dtype=torch.int32, device=device)
+
+    def fn(s, m):
+        z = splitmix(seed, stream, torch.arange(s, s + m, dtype=torch.int64, device=device))
+        return (torch.remainder(_srl(z, 32), hi - lo + 1) + lo).to(torch.int32)
+    _fill(out, fn)
+    return out.view(*shape)
+
+
+def sp24_pairs(M, K, seed, stream=STREAM_POS, device="cpu") -> torch.Tensor:
+    """index of the kept pair (0..5 into PAIRS) for every (row, group): shape (M, K/4) uint8."""
+    n = M * (K // 4)
+    out = torch.empty(n, dtype=torch.uint8, device=device)
+
+    def fn(s, m):
+        z = splitmix(seed, stream, torch.arange(s, s + m, dtype=torch.int64, device=device))
+        return torch.remainder(_srl(z, 32), 6).to(torch.uint8)
+    _fill(out, fn)
+    return out.view(M, K // 4)
+
+
+def sp24_canonical_meta(pairs: torch.Tensor) -> torch.Tensor:
+    """canonical metadata words (M, K/32) int32 from pair indices: nibble = i0 | i1 << 2 at
+    bits 4*(g%8) of word g/8.  Bit packing only."""
+    nib_table = torch.tensor([i0 | (i1 << 2) for i0, i1 in PAIRS], dtype=torch.int64, device=pairs.device)
+    nib = nib_table[pairs.long()]                               # (M, G)
+    M, G = nib.shape
+    nib = nib.view(M, G // 8, 8)
+    shifts = (4 * torch.arange(8, device=pairs.device, dtype=torch.int64)).view(1, 1, 8)
+    words = (nib << shifts).sum(dim=2)                          # < 2^32
+    words = torch.where(words >= (1 << 31), words - (1 << 32), words)
+    return words.to(torch.int32)
+
+
+def sp24_problem(M, K, seed, fmt="f16", device="cpu"):
+    """C5-style 2:4 operand: (vals (M, K/2), canonical meta (M, K/32) int32).
+    positions uniform over the 6 pairs; values N(0,1) with zero-redraw (never +-0)."""
+    pairs = sp24_pairs(M, K, seed, STREAM_POS, device)
+    vals = normal_matrix((M, K // 2), fmt, seed, STREAM_SPVAL, device, redraw_zero=True)
+    return vals, sp24_canonical_meta(pairs)
