@@ -1,0 +1,197 @@
+/*
+ * tcx.h — C ABI of the tcx library (libtcx.so): the tensor-core fused multiply-accumulate
+ *          D = A x B + C on B200 (sm_100a), dense and 2:4 structured-sparse.
+ *
+ * Source of every operation: arXiv 2206.02874, "Dissecting Tensor Cores via
+ * Microbenchmarks" (the paper; cited as PAPER.md:<line>):
+ *   - the MMA problem D = A x B + C, A m x k, B k x n, C the accumulator   PAPER.md:112 (§II-A)
+ *   - the mma instruction's "row.col" operand layout (only scheme)
+ *   - 2:4 sparse mma.sp: sA = m x k/2 non-zeros + 2-bit index metadata e
+ *   - latency / throughput microbenchmark method (clock counters, ILP x warps)
+ *                                                                          PAPER.md:263-293
+ *   - element-wise numeric probes (mul / inner-product add / accumulate)
+ *
+ * Conventions for every call:
+ *   - Plain pointers and sizes only.  Device pointers must live on the caller's current CUDA
+ *     device; "stream" is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - All calls are asynchronous on `stream` except tcx_probe (synchronous).
+ *   - Argument errors are detected synchronously before any launch, with no side effects.
+ *     Launch failures return TCX_ERR_CUDA.  Asynchronous device faults surface at the
+ *     caller's next synchronisation (CUDA semantics).  tcx_last_error() returns a
+ *     thread-local text for the last non-OK status.
+ *   - The caller owns every buffer.  GEMM paths allocate no device memory.
+ *   - Layouts (the paper's "row.col"): A is M x K row-major (lda >= K); B is stored N x K
+ *     row-major (ldb >= K), i.e. K-major "col" B; C and D are M x N row-major.
+ *     C == NULL means C = 0 (not read).  D may alias C (same ld) for in-place use.
+ *   - Alignment: device pointers 16-byte aligned; lda*esize, ldb*esize, ldc*4, ldd*4 are
+ *     multiples of 16 bytes; K*esize is a multiple of 16 bytes.  Otherwise
+ *     TCX_ERR_MISALIGNED.
+ *   - Element types: F16 = IEEE binary16, BF16 = bfloat16 (8,7), TF32 = (8,10) held in a
+ *     32-bit FP32 container whose low 13 bits MUST be zero (use tcx_round_tf32),
+ *     F32 = binary32, S8 = int8, S32 = int32 (Table `datatypes`).
+ *   - Numerics: FP inputs -> FP32 accumulate in the tensor cores; INT8 -> INT32 with
+ *     two's-complement wraparound (no saturation).  In tcx_gemm/tcx_gemm_sp24, C is added
+ *     to the FP32 accumulator in the epilogue with one RNE FP32 add (documented reading of
+ *     PAPER.md:112; DESIGN.md R-C4); in tcx_mma_tiles C is the MMA's own C operand, as in
+ *     the paper's probes.
+ */
+#ifndef TCX_H
+#define TCX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef enum {
+  TCX_OK = 0,
+  TCX_ERR_INVALID_VALUE = 1, /* bad size / NULL pointer / bad enum */
+  TCX_ERR_UNSUPPORTED = 2,   /* valid request this build does not implement (never garbage) */
+  TCX_ERR_MISALIGNED = 3,    /* pointer / leading-dimension alignment rule violated */
+  TCX_ERR_BAD_SPARSITY = 4,  /* reserved: sparsity violations are reported via d_first_bad */
+  TCX_ERR_NO_DEVICE = 5,     /* no CUDA device / driver */
+  TCX_ERR_ARCH = 6,          /* current device is not sm_100 */
+  TCX_ERR_CUDA = 7           /* a CUDA runtime/driver call failed (see tcx_last_error) */
+} tcx_status;
+
+typedef enum { TCX_F16 = 0, TCX_BF16 = 1, TCX_TF32 = 2, TCX_F32 = 3, TCX_S8 = 4, TCX_S32 = 5 } tcx_dtype;
+
+/* ---------------------------------------------------------------------------------------
+ * tcx_mma_tiles — a batch of `count` independent m x n x k tiles, one tensor-core MMA each
+ * (the paper's single mma instruction, at batch scale):
+ *     D_t = A_t x B_t + C_t,   t < count
+ * A: count x m x k row-major (ab elements);  B: count x n x k (n-major "col", ab elements);
+ * C, D: count x m x n row-major (cd elements).  C == NULL -> zeros.
+ * Supported (ab, cd, m, n, k):  (F16|BF16, F32, 16, 8, 16)  (TF32, F32, 16, 8, 8|16)
+ *                               (S8, S32, 16, 8, 32).  TF32 k=16 = two chained k=8 MMAs,
+ *                               the first's D feeding the second's C (DESIGN.md R-C15).
+ * count == 0 is a no-op.  Others -> TCX_ERR_UNSUPPORTED.
+ * ------------------------------------------------------------------------------------- */
+tcx_status tcx_mma_tiles(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, int64_t count,
+                         const void* A, const void* B, const void* C, void* D, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * tcx_gemm — dense D = A x B + C, M x N x K, layouts above.
+ * Supported: ab in {F16, BF16, TF32} with cd = F32;  ab = S8 with cd = S32.
+ * Any M, N >= 1 and K >= 1 subject to the alignment rules (ragged tiles are handled by
+ * TMA out-of-bounds zero fill and predicated stores).  M == 0 or N == 0 is a no-op;
+ * K == 0 gives D = C.
+ * ------------------------------------------------------------------------------------- */
+tcx_status tcx_gemm(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
+                    const void* A, int64_t lda, const void* B, int64_t ldb,
+                    const void* C, int64_t ldc, void* D, int64_t ldd, void* stream);
+
+/* kernel-configuration override for tests and the microbenchmark (0 = library default). */
+typedef struct {
+  int cta_group;   /* 1 or 2 (CTA pair, tcgen05 cta_group::2) */
+  int max_ctas;    /* cap on persistent CTAs (0 = all SMs) */
+  int reserved[6];
+} tcx_gemm_opts;
+tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
+                       const void* A, int64_t lda, const void* B, int64_t ldb,
+                       const void* C, int64_t ldc, void* D, int64_t ldd,
+                       const tcx_gemm_opts* opts, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * 2:4 structured sparsity: "for every four consecutive elements along
+ * the K dimension, there are two non-zero values"; sA is m x k/2; each kept element has a
+ * 2-bit index (00..11).
+ *
+ * Canonical metadata (the API format): uint32 words, K/32 per row, row-major (M x K/32).
+ * Group g (dense columns 4g..4g+3) is the nibble at bits 4*(g % 8) of word g / 8;
+ * nibble = i0 | i1 << 2 with 0 <= i0 < i1 <= 3 (lowest-order bit pair = first kept
+ * element).  Kept values are stored in order i0, i1.
+ *
+ * tcx_sp24_compress: dense A (M x K, lda) -> A_vals (M x K/2, row-major, ld = K/2) +
+ *   meta_canon.  Each group keeps its <=2 nonzeros (+-0 is zero, NaN is nonzero); groups
+ *   with fewer are padded with the lowest free indices.  A group with >2 nonzeros is a
+ *   violation: d_first_bad (device int64[2], written asynchronously) receives {row, group}
+ *   of the first violation in row-major order, or {-1, -1}.  K % 32 == 0.
+ * tcx_sp24_meta_hw_bytes / tcx_sp24_pack_meta: canonical -> the opaque hardware metadata
+ *   image consumed by tcx_gemm_sp24 (tensor-memory interleaved layout).
+ *   A nibble with i0 >= i1 is a violation reported through d_first_bad the same way.
+ *   M % 128 == 0 and K % 128 == 0 for the packer (pad rows / K otherwise).
+ * tcx_gemm_sp24: D = expand(A_vals, meta) x B + C.  ab = F16 or BF16, cd = F32.
+ *   A_vals: M x K/2 (lda_vals >= K/2); meta_hw from tcx_sp24_pack_meta for the same M, K;
+ *   B: N x K; C, D: M x N.  M % 128 == 0, K % 128 == 0, N % 16 == 0 required
+ *   (else TCX_ERR_UNSUPPORTED).
+ * ------------------------------------------------------------------------------------- */
+tcx_status tcx_sp24_compress(tcx_dtype ab, int64_t M, int64_t K, const void* A_dense, int64_t lda,
+                             void* A_vals, uint32_t* meta_canon, int64_t* d_first_bad, void* stream);
+size_t tcx_sp24_meta_hw_bytes(tcx_dtype ab, int64_t M, int64_t K);
+tcx_status tcx_sp24_pack_meta(tcx_dtype ab, int64_t M, int64_t K, const uint32_t* meta_canon,
+                              void* meta_hw, int64_t* d_first_bad, void* stream);
+tcx_status tcx_gemm_sp24(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
+                         const void* A_vals, int64_t lda_vals, const void* meta_hw,
+                         const void* B, int64_t ldb, const void* C, int64_t ldc,
+                         void* D, int64_t ldd, void* stream);
+
+/* tcx_round_tf32: out[i] = FP32 -> TF32 round-to-nearest-even of in[i] (low 13 bits
+ * cleared; NaN/Inf unchanged; a carry out of max-finite becomes Inf).  in may equal out. */
+tcx_status tcx_round_tf32(const float* in, float* out, int64_t n, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * tcx_probe — the paper's microbenchmark method on sm_100a:
+ *   each issuer runs ITERS iterations of ILP independent MMAs (iteration-dependent chains)
+ *   with a warp sync per iteration, timed with the SM clock counter.
+ *   latency   = cycles / ITERS
+ *   throughput = issuers * ILP * m*n*k / latency  [FMA/clk/SM]
+ * kinds:
+ *   TCX_PROBE_MMA_SYNC     legacy warp mma.sync (the paper's instruction), `warps` warps of
+ *                          one CTA (one CTA per SM if ctas_per_sm... = 1 CTA on 1 SM)
+ *   TCX_PROBE_MMA_SP_SYNC  legacy mma.sp (2:4), same harness
+ *   TCX_PROBE_TC05         tcgen05.mma issued by one thread; ILP = independent accumulators
+ *                          in flight per commit; `warps` = issuing CTAs per SM (1)
+ *   TCX_PROBE_TC05_SP      tcgen05.mma.sp
+ * Synchronous; allocates and frees its own scratch.  Shapes not implemented ->
+ * TCX_ERR_UNSUPPORTED.
+ * ------------------------------------------------------------------------------------- */
+typedef enum { TCX_PROBE_MMA_SYNC = 0, TCX_PROBE_MMA_SP_SYNC = 1, TCX_PROBE_TC05 = 2,
+               TCX_PROBE_TC05_SP = 3 } tcx_probe_kind;
+typedef struct {
+  int kind;          /* tcx_probe_kind */
+  int ab, cd;        /* tcx_dtype */
+  int m, n, k;       /* instruction shape (k = logical k for sparse) */
+  int cta_group;     /* tcgen05 only: 1 or 2 */
+  int warps;         /* mma.sync: warps per CTA; tcgen05: unused (1 issuer per CTA) */
+  int ilp;           /* independent MMAs per iteration */
+  int iters;         /* timed iterations */
+  int repeats;       /* repeated launches; min and median reported */
+  int num_sms;       /* CTAs launched (one per SM; 1 = the paper's single-SM setting) */
+} tcx_probe_config;
+typedef struct {
+  double cycles_per_iter_min, cycles_per_iter_median;
+  double latency_cycles;          /* = cycles_per_iter_median */
+  double fma_per_clk_per_sm;      /* issuers * ilp * m*n*k / latency */
+  double sm_mhz;                  /* measured: clock64 delta / globaltimer delta */
+  double ns_per_iter;
+  int64_t iters;
+  uint32_t sink;                  /* data-dependence sink (keeps the MMAs alive) */
+} tcx_probe_result;
+tcx_status tcx_probe(int device, const tcx_probe_config* cfg, tcx_probe_result* out);
+
+/* numeric probe through tcgen05: the same tile batch as tcx_mma_tiles (F16/BF16 m16n8k16,
+ * TF32 m16n8k8|16), but each group of 8 tiles is packed block-diagonally into one
+ * M=128,N=64 tcgen05.mma with C preloaded into tensor memory. */
+tcx_status tcx_mma_tiles_tc05(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, int64_t count,
+                              const void* A, const void* B, const void* C, void* D, void* stream);
+
+/* ------------------------------------------------------------------------------------- */
+const char* tcx_status_string(tcx_status s);
+const char* tcx_last_error(void);          /* thread-local detail of the last non-OK status */
+const char* tcx_version(void);
+/* number of kernels this library has launched in this process (all devices, all threads) */
+uint64_t tcx_launch_count(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCX_H */

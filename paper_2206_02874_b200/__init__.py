@@ -1,0 +1,229 @@
+"""paper_2206_02874_b200 — Python binding of libtcx.so (the B200 tensor-core MMA library).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels behind the
+C ABI declared in include/tcx.h.  torch supplies device memory and streams.  There is no
+CPU fallback: if libtcx.so is missing or a call fails, an exception is raised.
+
+Functions (same names as the C ABI, minus the ``tcx_`` prefix):
+  mma_tiles(A, B, C, D=None)            batch of m16n8k16 / m16n8k8|16 (tf32) / m16n8k32 (s8) tiles
+  mma_tiles_tc05(A, B, C, D=None)       the same tiles through tcgen05 (C preloaded in TMEM)
+  gemm(A, B, C=None, D=None, ...)       dense D = A @ B^T-stored + C   (B is N x K, "col")
+  sp24_compress(A_dense)                -> (vals, meta_canon)
+  sp24_pack_meta(meta_canon, M, K)      -> meta_hw
+  gemm_sp24(vals, meta_hw, B, C, D, K)  2:4 sparse D = expand(vals, meta) x B + C
+  round_tf32(x)                         FP32 -> TF32 RNE (FP32 storage)
+  probe(config dict)                    clock-counter latency/throughput
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtcx.so")
+
+F16, BF16, TF32, F32, S8, S32 = 0, 1, 2, 3, 4, 5
+_STATUS = {0: "TCX_OK", 1: "TCX_ERR_INVALID_VALUE", 2: "TCX_ERR_UNSUPPORTED", 3: "TCX_ERR_MISALIGNED",
+           4: "TCX_ERR_BAD_SPARSITY", 5: "TCX_ERR_NO_DEVICE", 6: "TCX_ERR_ARCH", 7: "TCX_ERR_CUDA"}
+
+EXPORTS = ["tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
+           "tcx_sp24_meta_hw_bytes", "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_round_tf32", "tcx_probe",
+           "tcx_status_string", "tcx_last_error", "tcx_version", "tcx_launch_count"]
+
+
+class TcxError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class GemmOpts(ctypes.Structure):
+    _fields_ = [("cta_group", ctypes.c_int), ("max_ctas", ctypes.c_int), ("reserved", ctypes.c_int * 6)]
+
+
+class ProbeConfig(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("kind", "ab", "cd", "m", "n", "k", "cta_group", "warps", "ilp",
+                                             "iters", "repeats", "num_sms")]
+
+
+class ProbeResult(ctypes.Structure):
+    _fields_ = [("cycles_per_iter_min", ctypes.c_double), ("cycles_per_iter_median", ctypes.c_double),
+                ("latency_cycles", ctypes.c_double), ("fma_per_clk_per_sm", ctypes.c_double),
+                ("sm_mhz", ctypes.c_double), ("ns_per_iter", ctypes.c_double), ("iters", ctypes.c_int64),
+                ("sink", ctypes.c_uint32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libtcx.so (fails loudly if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libtcx.so not found at {LIB_PATH}; run `python -m paper_2206_02874_b200.build`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    L.tcx_mma_tiles.argtypes = [i32, i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]
+    L.tcx_mma_tiles_tc05.argtypes = [i32, i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]
+    L.tcx_gemm.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
+    L.tcx_gemm_ex.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, ctypes.POINTER(GemmOpts), vp]
+    L.tcx_sp24_compress.argtypes = [i32, i64, i64, vp, i64, vp, vp, vp, vp]
+    L.tcx_sp24_meta_hw_bytes.argtypes = [i32, i64, i64]
+    L.tcx_sp24_meta_hw_bytes.restype = ctypes.c_size_t
+    L.tcx_sp24_pack_meta.argtypes = [i32, i64, i64, vp, vp, vp, vp]
+    L.tcx_gemm_sp24.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, vp, i64, vp, i64, vp, i64, vp]
+    L.tcx_round_tf32.argtypes = [vp, vp, i64, vp]
+    L.tcx_probe.argtypes = [i32, ctypes.POINTER(ProbeConfig), ctypes.POINTER(ProbeResult)]
+    L.tcx_status_string.restype = ctypes.c_char_p
+    L.tcx_last_error.restype = ctypes.c_char_p
+    L.tcx_version.restype = ctypes.c_char_p
+    L.tcx_launch_count.restype = ctypes.c_uint64
+    for f in ("tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
+              "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_round_tf32", "tcx_probe"):
+        getattr(L, f).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(st):
+    if st != 0:
+        raise TcxError(st, lib().tcx_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(t=None):
+    dev = t.device if t is not None else torch.device("cuda")
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def launch_count() -> int:
+    return int(lib().tcx_launch_count())
+
+
+_TORCH_AB = {torch.float16: F16, torch.bfloat16: BF16, torch.int8: S8}
+
+
+def ab_code(t: torch.Tensor, tf32: bool = False) -> int:
+    if t.dtype == torch.float32:
+        if not tf32:
+            raise TypeError("float32 operands are TF32 inputs: pass tf32=True (values must be TF32-representable)")
+        return TF32
+    return _TORCH_AB[t.dtype]
+
+
+def _dev_check(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("tcx operates on CUDA tensors only (no CPU fallback)")
+
+
+# ---------------------------------------------------------------------------------------- tiles
+def mma_tiles(A, B, C=None, D=None, tf32=False, tc05=False):
+    """D_t = A_t B_t + C_t for A (count, 16, k), B (count, 8, k), C/D (count, 16, 8)."""
+    _dev_check(A, B, C, D)
+    ab = ab_code(A, tf32)
+    count, m, k = A.shape
+    n = B.shape[1]
+    cd = S32 if ab == S8 else F32
+    if D is None:
+        D = torch.empty((count, m, n), dtype=torch.int32 if cd == S32 else torch.float32, device=A.device)
+    fn = lib().tcx_mma_tiles_tc05 if tc05 else lib().tcx_mma_tiles
+    _check(fn(ab, cd, m, n, k, count, _ptr(A), _ptr(B), _ptr(C), _ptr(D), _stream(A)))
+    return D
+
+
+def mma_tiles_tc05(A, B, C=None, D=None, tf32=False):
+    return mma_tiles(A, B, C, D, tf32=tf32, tc05=True)
+
+
+# ---------------------------------------------------------------------------------------- GEMM
+def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0):
+    """Dense D = A x B + C with A (M, K), B stored (N, K) ("row.col"), C/D (M, N)."""
+    _dev_check(A, B, C, D)
+    ab = ab_code(A, tf32)
+    M, K = A.shape
+    N = B.shape[0]
+    cd = S32 if ab == S8 else F32
+    if D is None:
+        D = torch.empty((M, N), dtype=torch.int32 if cd == S32 else torch.float32, device=A.device)
+    opts = GemmOpts(cta_group, max_ctas)
+    _check(lib().tcx_gemm_ex(ab, cd, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
+                             _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
+                             ctypes.byref(opts), _stream(A)))
+    return D
+
+
+# ---------------------------------------------------------------------------------------- sparse
+def sp24_compress(A_dense):
+    """dense (M, K) 2:4 matrix -> (vals (M, K/2), meta_canon (M, K/32) int32).
+    Raises ValueError naming the first (row, group) with more than 2 nonzeros."""
+    _dev_check(A_dense)
+    ab = ab_code(A_dense)
+    M, K = A_dense.shape
+    vals = torch.empty((M, K // 2), dtype=A_dense.dtype, device=A_dense.device)
+    meta = torch.empty((M, K // 32), dtype=torch.int32, device=A_dense.device)
+    bad = torch.empty(2, dtype=torch.int64, device=A_dense.device)
+    _check(lib().tcx_sp24_compress(ab, M, K, _ptr(A_dense), A_dense.stride(0), _ptr(vals), _ptr(meta),
+                                   _ptr(bad), _stream(A_dense)))
+    r, g = bad.tolist()
+    if r >= 0:
+        raise ValueError(f"2:4 violation at row {r}, group {g}")
+    return vals, meta
+
+
+def sp24_meta_hw_bytes(M, K, ab=F16):
+    return int(lib().tcx_sp24_meta_hw_bytes(ab, M, K))
+
+
+def sp24_pack_meta(meta_canon, M, K, ab=F16, check=True):
+    _dev_check(meta_canon)
+    nbytes = sp24_meta_hw_bytes(M, K, ab)
+    hw = torch.empty(nbytes, dtype=torch.uint8, device=meta_canon.device)
+    bad = torch.empty(2, dtype=torch.int64, device=meta_canon.device)
+    _check(lib().tcx_sp24_pack_meta(ab, M, K, _ptr(meta_canon), _ptr(hw), _ptr(bad), _stream(meta_canon)))
+    if check:
+        r, g = bad.tolist()
+        if r >= 0:
+            raise ValueError(f"bad metadata nibble at row {r}, group {g}")
+    return hw
+
+
+def gemm_sp24(vals, meta_hw, B, C=None, D=None):
+    """D = expand(vals, meta) x B + C; vals (M, K/2), B (N, K)."""
+    _dev_check(vals, meta_hw, B, C, D)
+    ab = ab_code(vals)
+    M = vals.shape[0]
+    N, K = B.shape
+    if D is None:
+        D = torch.empty((M, N), dtype=torch.float32, device=vals.device)
+    _check(lib().tcx_gemm_sp24(ab, F32, M, N, K, _ptr(vals), vals.stride(0), _ptr(meta_hw), _ptr(B), B.stride(0),
+                               _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0), _stream(vals)))
+    return D
+
+
+def round_tf32(x, out=None):
+    _dev_check(x, out)
+    if out is None:
+        out = torch.empty_like(x)
+    _check(lib().tcx_round_tf32(_ptr(x), _ptr(out), x.numel(), _stream(x)))
+    return out
+
+
+# ---------------------------------------------------------------------------------------- probe
+PROBE_KINDS = {"mma_sync": 0, "mma_sp_sync": 1, "tc05": 2, "tc05_sp": 3}
+
+
+def probe(kind="mma_sync", ab=F16, cd=F32, m=16, n=8, k=16, cta_group=1, warps=1, ilp=1, iters=1024,
+          repeats=5, num_sms=1, device=-1):
+    cfg = ProbeConfig(PROBE_KINDS[kind] if isinstance(kind, str) else kind, ab, cd, m, n, k, cta_group, warps, ilp,
+                      iters, repeats, num_sms)
+    res = ProbeResult()
+    _check(lib().tcx_probe(device, ctypes.byref(cfg), ctypes.byref(res)))
+    return {f: getattr(res, f) for f, _ in ProbeResult._fields_}

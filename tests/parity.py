@@ -1,0 +1,78 @@
+"""Parity helpers shared by the GPU tests (tests only; imports the oracle, never the reverse).
+
+The FP bar (BASELINE.json north_star), written out once here and used by every FP test:
+    |D - D_ref| <= (K + 2) * 2^-23 * (sum_k |a_ik b_kj| + |c_ij|)      per element,
+with K the logical K and D_ref the exact-plus-one-RNE oracle.  Integer / index work: bit-exact.
+"""
+import numpy as np
+import torch
+
+import oracle as O
+
+TORCH2ORACLE = {torch.float16: O.F16, torch.bfloat16: O.BF16, torch.float32: O.TF32, torch.int8: O.S8}
+
+
+def host_bits(t: torch.Tensor) -> np.ndarray:
+    """the exact bytes of a tensor as an unsigned numpy array (16-bit types -> uint16 etc.)"""
+    t = t.detach().contiguous().cpu()
+    if t.dtype in (torch.float16, torch.bfloat16):
+        return t.view(torch.int16).numpy().view(np.uint16)
+    if t.dtype == torch.float32:
+        return t.view(torch.int32).numpy().view(np.uint32)
+    if t.dtype == torch.int32:
+        return t.numpy().view(np.uint32)
+    if t.dtype == torch.int8:
+        return t.numpy()
+    raise TypeError(t.dtype)
+
+
+def fp_bound_check(got_bits: np.ndarray, ref_bits: np.ndarray, absv: np.ndarray, K: int, what=""):
+    """assert the north_star bound; returns the max normalised error |D-Dref| / (2^-23 (sum|ab|+|c|))."""
+    got = got_bits.view(np.float32).astype(np.float64)
+    ref = ref_bits.view(np.float32).astype(np.float64)
+    assert np.all(np.isfinite(got)), f"{what}: non-finite output"
+    err = np.abs(got - ref)
+    scale = (2.0 ** -23) * absv
+    bound = (K + 2) * scale
+    bad = err > bound
+    if bad.any():
+        i = int(np.argmax(bad))
+        raise AssertionError(f"{what}: {int(bad.sum())} elements exceed the FP bound; first at flat {i}: "
+                             f"got {got.flat[i]!r} ref {ref.flat[i]!r} bound {bound.flat[i]!r}")
+    with np.errstate(divide="ignore", invalid="ignore"):
+        norm = np.where(scale > 0, err / scale, 0.0)
+    return float(norm.max()) if norm.size else 0.0
+
+
+def gemm_sample_coords(M, N, tile_m, tile_n, nsamp=65536, seed=0, extra_rows=()):
+    """the SURVEY §8(d) sample: the 4 corners of every CTA output tile, 256 seeded columns of
+    each extra row (shard boundaries), then uniform (i, j) until nsamp."""
+    rng = np.random.default_rng(seed)
+    rows, cols = [], []
+    for m0 in range(0, M, tile_m):
+        m1 = min(M, m0 + tile_m) - 1
+        for n0 in range(0, N, tile_n):
+            n1 = min(N, n0 + tile_n) - 1
+            rows += [m0, m0, m1, m1]
+            cols += [n0, n1, n0, n1]
+    for r in extra_rows:
+        c = rng.integers(0, N, 256)
+        rows += [r] * 256
+        cols += c.tolist()
+    need = max(0, nsamp - len(rows))
+    rows += rng.integers(0, M, need).tolist()
+    cols += rng.integers(0, N, need).tolist()
+    return np.array(rows, np.int64), np.array(cols, np.int64)
+
+
+def check_gemm_samples(ab, A, B, C, D, rows, cols, K, what=""):
+    """oracle on sampled coordinates (host copies of the very bytes the GPU consumed)."""
+    Ah, Bh = host_bits(A), host_bits(B)
+    Ch = host_bits(C) if C is not None else None
+    ref, absv = O.gemm_samples(ab, Ah, Bh, Ch, rows, cols)
+    got = host_bits(D)[rows, cols]
+    if ab == O.S8:
+        mism = np.nonzero(got != ref)[0]
+        assert mism.size == 0, f"{what}: {mism.size} int mismatches, first at {(rows[mism[0]], cols[mism[0]])}"
+        return 0.0
+    return fp_bound_check(got, ref, absv, K, what)

@@ -1,0 +1,156 @@
+"""tcx_gemm (tcgen05 dense) vs the oracle: small shapes whole-matrix, ragged tails, both CTA
+modes, every kind; BASELINE configs[2] (C3 BF16/TF32 8192^3) and configs[3] (C4 INT8 16384^3)
+at full size on >= 65,536 sampled outputs + full-coverage properties."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import tcxgen
+import paper_2206_02874_b200 as tcx
+from parity import host_bits, fp_bound_check, gemm_sample_coords, check_gemm_samples, TORCH2ORACLE
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _problem(M, N, K, fmt, seed=0, with_c=True):
+    if fmt == "s8":
+        A = tcxgen.int8_matrix((M, K), seed, tcxgen.STREAM_A, DEV)
+        B = tcxgen.int8_matrix((N, K), seed, tcxgen.STREAM_B, DEV)
+        C = tcxgen.int32_matrix((M, N), seed, tcxgen.STREAM_C, device=DEV) if with_c else None
+        return A, B, C
+    A = tcxgen.normal_matrix((M, K), fmt, seed, tcxgen.STREAM_A, DEV)
+    B = tcxgen.normal_matrix((N, K), fmt, seed, tcxgen.STREAM_B, DEV)
+    C = tcxgen.normal_matrix((M, N), "f32", seed, tcxgen.STREAM_C, DEV) if with_c else None
+    return A, B, C
+
+
+def _full_check(fmt, A, B, C, D):
+    M, K = A.shape
+    N = B.shape[0]
+    ii, jj = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+    ab = TORCH2ORACLE[A.dtype]
+    return check_gemm_samples(ab, A, B, C, D, ii.ravel(), jj.ravel(), K, f"gemm {fmt} {M}x{N}x{K}")
+
+
+SMALL = [(256, 256, 128), (128, 256, 64), (512, 512, 512), (200, 136, 72), (264, 520, 40), (1, 4, 8), (384, 16, 1024)]
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("fmt", ["bf16", "f16", "tf32", "s8"])
+@pytest.mark.parametrize("shape", SMALL)
+def test_gemm_small_whole_matrix(fmt, cg, shape):
+    M, N, K = shape
+    if fmt == "s8":
+        K = max(16, (K + 15) // 16 * 16)
+    A, B, C = _problem(M, N, K, fmt, seed=M + N + K)
+    D = tcx.gemm(A, B, C, tf32=(fmt == "tf32"), cta_group=cg)
+    torch.cuda.synchronize()
+    _full_check(fmt, A, B, C, D)
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("fmt", ["bf16", "tf32"])
+def test_gemm_integer_valued_bit_exact(fmt, cg):
+    """|a|,|b| <= 8 integers: exact sums -> bit-exact on every path (pins indexing/layout)."""
+    M, N, K = 512, 768, 320
+    dt = {"bf16": torch.bfloat16, "tf32": torch.float32}[fmt]
+    A = tcxgen.int32_matrix((M, K), 1, 1, -8, 8, DEV).to(dt)
+    B = tcxgen.int32_matrix((N, K), 1, 2, -8, 8, DEV).to(dt)
+    C = tcxgen.int32_matrix((M, N), 1, 3, -1000, 1000, DEV).to(torch.float32)
+    D = tcx.gemm(A, B, C, tf32=(fmt == "tf32"), cta_group=cg)
+    ref = (A.double() @ B.double().T + C.double())
+    torch.cuda.synchronize()
+    assert torch.equal(D.double(), ref)
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+def test_gemm_persistent_many_tiles_per_cta(cg):
+    """few CTAs, many tiles each: exercises the smem ring and TMEM double-buffer phases."""
+    M, N, K = 1024, 1280, 1024
+    A, B, C = _problem(M, N, K, "bf16", seed=3)
+    D = tcx.gemm(A, B, C, cta_group=cg, max_ctas=2 * cg)
+    D2 = tcx.gemm(A, B, C, cta_group=cg)
+    torch.cuda.synchronize()
+    assert torch.equal(D.view(torch.int32), D2.view(torch.int32))   # same per-element arithmetic
+    rows, cols = gemm_sample_coords(M, N, 128 * cg, 256, nsamp=8192)
+    check_gemm_samples(O.BF16, A, B, C, D, rows, cols, K, "persistent")
+
+
+def test_gemm_no_c_k0_and_errors():
+    A, B, _ = _problem(256, 256, 64, "bf16", seed=4, with_c=False)
+    D = tcx.gemm(A, B, None)
+    torch.cuda.synchronize()
+    _full_check("bf16", A, B, None, D)
+    # K == 0: D = C
+    C = torch.randn(64, 32, device=DEV)
+    D0 = tcx.gemm(A[:64, :0], B[:32, :0], C)
+    torch.cuda.synchronize()
+    assert torch.equal(D0, C)
+    # misaligned K (K*2 % 16 != 0) is rejected, not computed
+    A2 = torch.zeros(64, 12, dtype=torch.bfloat16, device=DEV)
+    B2 = torch.zeros(64, 12, dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(tcx.TcxError):
+        tcx.gemm(A2, B2)
+
+
+def test_gemm_determinism_and_cta_modes_agree():
+    A, B, C = _problem(1024, 1024, 2048, "bf16", seed=6)
+    D1 = tcx.gemm(A, B, C, cta_group=1)
+    D2 = tcx.gemm(A, B, C, cta_group=2)
+    D3 = tcx.gemm(A, B, C, cta_group=2)
+    torch.cuda.synchronize()
+    assert torch.equal(D2.view(torch.int32), D3.view(torch.int32))
+    # both modes are inside the bound; they need not be bitwise equal
+    rows, cols = gemm_sample_coords(1024, 1024, 256, 256, nsamp=4096)
+    check_gemm_samples(O.BF16, A, B, C, D1, rows, cols, 2048, "cg1")
+
+
+def _float64_full_coverage(A, B, C, D, K):
+    """every output vs float64 A.B (a library routine used as a check, not the oracle):
+    |D - ref64| <= (K+2) 2^-23 (|A||B| + |C|) + K 2^-52 (|A||B|) for all M*N outputs."""
+    Ad, Bd = A.double(), B.double()
+    ref = Ad @ Bd.T
+    mag = Ad.abs() @ Bd.abs().T
+    if C is not None:
+        ref += C.double()
+        mag += C.double().abs()
+    err = (D.double() - ref).abs()
+    bound = (K + 2) * 2.0 ** -23 * mag + K * 2.0 ** -52 * mag
+    bad = int((err > bound).sum())
+    assert bad == 0, f"{bad} outputs exceed the bound"
+    return float((err / (2.0 ** -23 * mag).clamp_min(1e-300)).max())
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "tf32"])
+def test_config3_full_size(fmt):
+    """BASELINE configs[2]: M=N=K=8192, A,B N(0,1) (BF16, or FP32 rounded to TF32), C FP32 zeros."""
+    M = N = K = 8192
+    A, B, _ = _problem(M, N, K, fmt, seed=0, with_c=False)
+    C = torch.zeros(M, N, dtype=torch.float32, device=DEV)
+    D = tcx.gemm(A, B, C, tf32=(fmt == "tf32"))
+    torch.cuda.synchronize()
+    rows, cols = gemm_sample_coords(M, N, 256, 256, nsamp=65536)
+    norm = check_gemm_samples(TORCH2ORACLE[A.dtype], A, B, C, D, rows, cols, K, f"C3 {fmt}")
+    assert norm < K + 2
+    _float64_full_coverage(A, B, C, D, K)
+
+
+def test_config4_full_size_int8_bit_exact():
+    """BASELINE configs[3]: INT8 16384^3, C int32 U[-2^20, 2^20]: bit-exact; Freivalds mod 2^32
+    on all outputs."""
+    M = N = K = 16384
+    A, B, C = _problem(M, N, K, "s8", seed=0)
+    D = tcx.gemm(A, B, C)
+    torch.cuda.synchronize()
+    rows, cols = gemm_sample_coords(M, N, 256, 256, nsamp=65536)
+    check_gemm_samples(O.S8, A, B, C, D, rows, cols, K, "C4")
+    # Freivalds, exact mod 2^32: float64 products are exact here (|D r| < 2^52, |A (B r)| < 2^49)
+    g = torch.Generator(device=DEV).manual_seed(1)
+    Dd, Ad, Bd, Cd = D.double(), A.double(), B.double(), C.double()
+    for _ in range(8):
+        r = torch.randint(0, 128, (N, 1), device=DEV, generator=g).double()
+        lhs = (Dd @ r).long()
+        rhs = (Ad @ (Bd @ r) + Cd @ r).long()
+        assert torch.equal((lhs - rhs) & 0xFFFFFFFF, torch.zeros_like(lhs))
