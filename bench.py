@@ -1,0 +1,533 @@
+#!/usr/bin/env python
+"""tcx benchmark — BASELINE.json metric: dense & 2:4-sparse MMA TFLOP/s (INT8 TOPS) per B200,
+% of tensor-core peak.
+
+A step is one call of the hot path on its config's synthetic input, resident in HBM:
+  c3     (default) dense BF16 GEMM M=N=K=8192, C FP32 zeros (real buffer), FP32 D  (configs[2])
+  c3tf32 the same shape with TF32 inputs                                             (configs[2])
+  c4     INT8 GEMM M=N=K=16384, C int32 U[-2^20,2^20], INT32 D                        (configs[3])
+  c5     2:4 sparse FP16 GEMM M=65536, N=K=16384, C FP32 zeros                        (configs[4])
+  c1     4096 m16n8k16 FP16 tiles (HBM-bound; GB/s)                                   (configs[0])
+At N=1 the default run also measures c3tf32 / c4 / c5 / c1 on rank 0 ("also" key).
+Multi-GPU (torchrun): rows of A, C, D are sharded across ranks (strong scaling, total work
+fixed); B is replicated by one NCCL broadcast before timing; time = max over ranks.
+
+--impl reference times the CPU oracle (oracle/, exact Kulisch accumulation) on a bounded sample
+of the same workload, on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+
+L2_BYTES = 126 * 1024 * 1024
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"bf16": d["bf16_tflops"], "bf16_sustained": d.get("bf16_tflops_sustained"), "hbm": d["hbm_gbs"],
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"bf16": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# nominal dense ratios vs bf16 (B200_PROFILING.md nominal table: tf32 1.1 vs 2.25; int8 = fp8 rate 4.5;
+# 2:4 sparse doubles the dense rate): peak for kind = measured bf16 peak x ratio
+KIND_RATIO = {"bf16": 1.0, "f16": 1.0, "tf32": 0.5, "s8": 2.0, "sp16": 2.0}
+
+
+class ClockSampler:
+    """nvidia-smi style clocks + throttle reasons sampled via NVML during the timed region."""
+
+    def __init__(self, index):
+        self.samples = []
+        self.on = False
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            log("nvml unavailable:", e)
+
+    def _run(self):
+        nv = self.nv
+        while self.on:
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.time(), mhz, rs))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        if self.ok:
+            self.on = True
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+
+    def stop(self):
+        if self.ok and self.on:
+            self.on = False
+            self.t.join()
+
+    def summary(self, t0, t1):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        nv = self.nv
+        inside = [s for s in self.samples if t0 <= s[0] <= t1] or self.samples[-3:]
+        names = {getattr(nv, "nvmlClocksEventReasonGpuIdle", 1): "gpu_idle",
+                 getattr(nv, "nvmlClocksEventReasonApplicationsClocksSetting", 2): "applications_clocks_setting",
+                 getattr(nv, "nvmlClocksEventReasonSwPowerCap", 4): "sw_power_cap",
+                 getattr(nv, "nvmlClocksEventReasonHwSlowdown", 8): "hw_slowdown",
+                 getattr(nv, "nvmlClocksEventReasonSyncBoost", 16): "sync_boost",
+                 getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 32): "sw_thermal_slowdown",
+                 getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 64): "hw_thermal_slowdown",
+                 getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 128): "hw_power_brake_slowdown"}
+        rs = set()
+        for _, _, r in inside:
+            for bit, nm in names.items():
+                if r & bit:
+                    rs.add(nm)
+        mhz = [s[1] for s in inside]
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(rs), "samples": len(inside)}
+
+
+# ----------------------------------------------------------------------------------- workloads
+class Work:
+    """one config on this rank: inputs resident in HBM, step() launches the hot path once."""
+
+    def __init__(self, cfg, rank, world, dev, seed=0):
+        import tcxgen
+        import paper_2206_02874_b200 as tcx
+        self.tcx, self.cfg, self.dev = tcx, cfg, dev
+        self.rank, self.world = rank, world
+        g = tcxgen
+        if cfg in ("c3", "c3tf32"):
+            M = N = K = 8192
+            fmt = "bf16" if cfg == "c3" else "tf32"
+            self.kind = fmt
+            self.shape = (M, N, K)
+            m0, m1 = self._rows(M)
+            self.A = g.normal_matrix((M, K), fmt, seed, g.STREAM_A, dev)[m0:m1].contiguous()
+            self.B = self._bcast(lambda: g.normal_matrix((N, K), fmt, seed, g.STREAM_B, dev))
+            self.C = torch.zeros(m1 - m0, N, dtype=torch.float32, device=dev)
+            self.D = torch.empty(m1 - m0, N, dtype=torch.float32, device=dev)
+            self.flops = 2.0 * (m1 - m0) * N * K
+            self.alg_bytes = self.A.numel() * self.A.element_size() + self.B.numel() * self.B.element_size() + 8 * (m1 - m0) * N
+            self.tf32 = fmt == "tf32"
+            self.kernel = "gemm_dense_kernel<2,%d>" % (0 if fmt == "bf16" else 1)
+            self.step = lambda: tcx.gemm(self.A, self.B, self.C, self.D, tf32=self.tf32)
+            self.unit, self.bound = "TFLOP/s", "tensor"
+        elif cfg == "c4":
+            M = N = K = 16384
+            self.kind = "s8"
+            self.shape = (M, N, K)
+            m0, m1 = self._rows(M)
+            self.A = g.int8_matrix((M, K), seed, g.STREAM_A, dev)[m0:m1].contiguous()
+            self.B = self._bcast(lambda: g.int8_matrix((N, K), seed, g.STREAM_B, dev))
+            self.C = g.int32_matrix((M, N), seed, g.STREAM_C, device=dev)[m0:m1].contiguous()
+            self.D = torch.empty(m1 - m0, N, dtype=torch.int32, device=dev)
+            self.flops = 2.0 * (m1 - m0) * N * K
+            self.alg_bytes = self.A.numel() + self.B.numel() + 8 * (m1 - m0) * N
+            self.kernel = "gemm_dense_kernel<2,2>"
+            self.step = lambda: tcx.gemm(self.A, self.B, self.C, self.D)
+            self.unit, self.bound = "TOPS", "tensor"
+        elif cfg == "c5":
+            M, N, K = 65536, 16384, 16384
+            self.kind = "sp16"
+            self.shape = (M, N, K)
+            m0, m1 = self._rows(M)
+            vals, meta = g.sp24_problem(M, K, seed, "f16", dev)
+            self.vals = vals[m0:m1].contiguous()
+            meta = meta[m0:m1].contiguous()
+            del vals
+            self.meta_hw = tcx.sp24_pack_meta(meta, m1 - m0, K)
+            del meta
+            self.B = self._bcast(lambda: g.normal_matrix((N, K), "f16", seed, g.STREAM_B, dev))
+            self.C = torch.zeros(m1 - m0, N, dtype=torch.float32, device=dev)
+            self.D = torch.empty(m1 - m0, N, dtype=torch.float32, device=dev)
+            self.flops = 2.0 * (m1 - m0) * N * K / 2          # effective (kept products); dense-eq = 2x
+            self.alg_bytes = self.vals.numel() * 2 + self.meta_hw.numel() + self.B.numel() * 2 + 8 * (m1 - m0) * N
+            self.kernel = "gemm_sp24_kernel"
+            self.step = lambda: tcx.gemm_sp24(self.vals, self.meta_hw, self.B, self.C, self.D)
+            self.unit, self.bound = "TFLOP/s", "tensor"
+        elif cfg == "c1":
+            count = 4096
+            self.kind = "f16"
+            self.shape = (count,)
+            copies = 64                                 # 64 x 7 MiB = 470 MB >> L2: reads are cold
+            self.As = [g.uniform_matrix((count, 16, 16), "f16", seed + i, g.STREAM_A, device=dev) for i in range(copies)]
+            self.Bs = [g.uniform_matrix((count, 8, 16), "f16", seed + i, g.STREAM_B, device=dev) for i in range(copies)]
+            self.Cs = [g.uniform_matrix((count, 16, 8), "f32", seed + i, g.STREAM_C, device=dev) for i in range(copies)]
+            self.Ds = [torch.empty(count, 16, 8, device=dev) for _ in range(copies)]
+            self.i = 0
+            self.flops = 4096.0 * count
+            self.alg_bytes = 1792 * count
+            self.kernel = "tiles16_kernel<0>"
+
+            def step():
+                j = self.i % copies
+                self.i += 1
+                tcx.mma_tiles(self.As[j], self.Bs[j], self.Cs[j], self.Ds[j])
+            self.step = step
+            self.unit, self.bound = "GB/s", "hbm"
+        else:
+            raise ValueError(cfg)
+
+    def _rows(self, M):
+        per = M // self.world
+        return self.rank * per, (self.rank + 1) * per
+
+    def _bcast(self, make):
+        import torch.distributed as dist
+        if self.world == 1:
+            return make()
+        t = make()               # every rank allocates B; rank 0's copy is the one broadcast
+        if self.rank != 0:
+            t.zero_()
+        dist.broadcast(t, src=0)
+        return t
+
+    def metric_value(self, seconds_per_step):
+        if self.unit == "GB/s":
+            return self.alg_bytes / seconds_per_step / 1e9
+        return self.flops / seconds_per_step / 1e12
+
+    # host-buffer end-to-end step through the public API: H2D of inputs, the call, D2H of D
+    def e2e_setup(self):
+        if self.cfg == "c1":
+            self.hA = self.As[0].cpu().pin_memory(); self.hB = self.Bs[0].cpu().pin_memory()
+            self.hC = self.Cs[0].cpu().pin_memory(); self.hD = torch.empty_like(self.Ds[0], device="cpu").pin_memory()
+            ins = [self.hA, self.hB, self.hC]
+        elif self.cfg == "c5":
+            self.hA = self.vals.cpu().pin_memory(); self.hM = self.meta_hw.cpu().pin_memory()
+            self.hB = self.B.cpu().pin_memory(); self.hC = self.C.cpu().pin_memory()
+            self.hD = torch.empty_like(self.D, device="cpu").pin_memory()
+            ins = [self.hA, self.hM, self.hB, self.hC]
+        else:
+            self.hA = self.A.cpu().pin_memory(); self.hB = self.B.cpu().pin_memory()
+            self.hC = self.C.cpu().pin_memory(); self.hD = torch.empty_like(self.D, device="cpu").pin_memory()
+            ins = [self.hA, self.hB, self.hC]
+        self.h2d = sum(t.numel() * t.element_size() for t in ins)
+        self.d2h = self.hD.numel() * self.hD.element_size()
+
+    def e2e_step(self):
+        tcx = self.tcx
+        if self.cfg == "c1":
+            A = self.hA.to(self.dev, non_blocking=True); B = self.hB.to(self.dev, non_blocking=True)
+            C = self.hC.to(self.dev, non_blocking=True)
+            D = tcx.mma_tiles(A, B, C)
+        elif self.cfg == "c5":
+            A = self.hA.to(self.dev, non_blocking=True); Mh = self.hM.to(self.dev, non_blocking=True)
+            B = self.hB.to(self.dev, non_blocking=True); C = self.hC.to(self.dev, non_blocking=True)
+            D = tcx.gemm_sp24(A, Mh, B, C)
+        else:
+            A = self.hA.to(self.dev, non_blocking=True); B = self.hB.to(self.dev, non_blocking=True)
+            C = self.hC.to(self.dev, non_blocking=True)
+            D = tcx.gemm(A, B, C, tf32=getattr(self, "tf32", False))
+        self.hD.copy_(D, non_blocking=True)
+
+
+def time_steps(work, steps, warmup, dist_on, sampler=None):
+    """W untimed warm-ups, then EXACTLY `steps` steps between barrier+sync; CUDA events on the
+    launching (current) stream; returns (ms_per_step on this rank, launches, t0, t1)."""
+    import paper_2206_02874_b200 as tcx
+    for _ in range(warmup):
+        work.step()
+    torch.cuda.synchronize()
+    if dist_on:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = tcx.launch_count()
+    t0 = time.time()
+    e0.record(stream)
+    for _ in range(steps):
+        work.step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t1 = time.time()
+    if dist_on:
+        torch.distributed.barrier()
+    launches = tcx.launch_count() - n0
+    return e0.elapsed_time(e1) / steps, launches, t0, t1
+
+
+def time_e2e(work, steps, warmup):
+    work.e2e_setup()
+    for _ in range(max(1, warmup)):
+        work.e2e_step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        work.e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def roofline(work, ms, pk):
+    if work.bound == "hbm":
+        ach = work.alg_bytes / (ms * 1e-3) / 1e9
+        peak = pk["hbm"]
+        unit = "GB/s"
+    else:
+        ach = work.flops / (ms * 1e-3) / 1e12
+        peak = pk["bf16"] * KIND_RATIO[work.kind]
+        unit = "TFLOP/s"
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(work.cfg)
+    return {"bound": work.bound, "achieved": round(ach, 2), "peak": round(peak, 2), "unit": unit,
+            "frac": round(ach / peak, 4), "traffic": traffic, "kernel": work.kernel,
+            "peak_source": pk["source"] + (" x nominal %s/bf16 ratio %.1f" % (work.kind, KIND_RATIO[work.kind])
+                                            if work.bound == "tensor" and KIND_RATIO[work.kind] != 1.0 else "")}
+
+
+# ----------------------------------------------------------------------------------- oracle baseline
+def oracle_sample(cfg, seconds=12.0, seed=0):
+    """time the CPU oracle (as it stands) on a bounded sample of the config; returns dict."""
+    import oracle as O
+    import tcxgen as g
+    cores = len(os.sched_getaffinity(0))
+    rng = np.random.default_rng(seed)
+    if cfg in ("c3", "c3tf32", "c4"):
+        M = N = K = 16384 if cfg == "c4" else 8192
+        fmt = {"c3": "bf16", "c3tf32": "tf32", "c4": "s8"}[cfg]
+        ab = {"bf16": O.BF16, "tf32": O.TF32, "s8": O.S8}[fmt]
+        # a sample of R rows x S cols of the same synthetic matrices (counter-based generator)
+        R, S = 16, 16
+
+        def rows_of(stream, idx, n_cols):
+            out = []
+            for r in idx:   # the exact row r of the synthetic matrix, by counters
+                if fmt == "s8":
+                    out.append(_counter_row_int8(seed, stream, int(r), n_cols))
+                else:
+                    out.append(_counter_row_fp(seed, stream, int(r), n_cols, fmt))
+            return np.stack(out)
+
+        t_total = 0.0
+        outputs = 0
+        while t_total < seconds:
+            ri = rng.integers(0, M, R); ci = rng.integers(0, N, S)
+            Ah = rows_of(g.STREAM_A, ri, K)
+            Bh = rows_of(g.STREAM_B, ci, K)
+            Ch = None
+            if cfg == "c4":
+                Ch = np.stack([_counter_row_int32(seed, g.STREAM_C, int(r), N)[ci] for r in ri]).astype(np.int32)
+            rr, cc = np.meshgrid(np.arange(R), np.arange(S), indexing="ij")
+            t0 = time.perf_counter()
+            O.gemm_samples(ab, Ah, Bh, Ch.view(np.uint32) if Ch is not None else None, rr.ravel(), cc.ravel(), cores)
+            t_total += time.perf_counter() - t0
+            outputs += R * S
+        ops = 2.0 * K * outputs
+        return {"value": ops / t_total / 1e12, "unit": "TOPS" if cfg == "c4" else "TFLOP/s", "cores": cores,
+                "kind": "oracle", "sample": f"{outputs} sampled outputs of the {M}x{N}x{K} {fmt} GEMM "
+                f"({outputs * K:.3g} exact MACs) in {t_total:.1f} s", "seconds": t_total}
+    if cfg == "c5":
+        M, N, K = 65536, 16384, 16384
+        R, S = 8, 16
+        t_total, outputs = 0.0, 0
+        while t_total < seconds:
+            ri = rng.integers(0, M, R); ci = rng.integers(0, N, S)
+            vals = np.stack([_counter_row_fp(seed, g.STREAM_SPVAL, int(r), K // 2, "f16", redraw=True) for r in ri])
+            meta = np.stack([_counter_meta_row(seed, int(r), K) for r in ri])
+            Bh = np.stack([_counter_row_fp(seed, g.STREAM_B, int(c), K, "f16") for c in ci])
+            t0 = time.perf_counter()
+            dense = O.sp24_expand(vals, meta, K)
+            rr, cc = np.meshgrid(np.arange(R), np.arange(S), indexing="ij")
+            O.gemm_samples(O.F16, dense, Bh, None, rr.ravel(), cc.ravel(), cores)
+            t_total += time.perf_counter() - t0
+            outputs += R * S
+        return {"value": 2.0 * (K // 2) * outputs / t_total / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                "sample": f"{outputs} sampled outputs of the {M}x{N}x{K} 2:4 FP16 GEMM in {t_total:.1f} s",
+                "seconds": t_total}
+    if cfg == "c1":
+        count = 4096
+        A = g.uniform_matrix((count, 16, 16), "f16", seed, g.STREAM_A)
+        B = g.uniform_matrix((count, 8, 16), "f16", seed, g.STREAM_B)
+        C = g.uniform_matrix((count, 16, 8), "f32", seed, g.STREAM_C)
+        hb = lambda t: t.view(torch.int16).numpy().view(np.uint16)
+        t0 = time.perf_counter()
+        n = 0
+        while time.perf_counter() - t0 < seconds:
+            O.tiles(O.F16, 16, 8, 16, hb(A), hb(B), C.view(torch.int32).numpy().view(np.uint32))
+            n += 1
+        dt = time.perf_counter() - t0
+        return {"value": 1792 * count * n / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                "sample": f"{n} whole C1 batches (4096 tiles) in {dt:.1f} s", "seconds": dt}
+    raise ValueError(cfg)
+
+
+def _counter_row_fp(seed, stream, r, n, fmt, redraw=False):
+    import tcxgen as g
+    v = g.to_format(g.normal(seed, stream, r * n, n), fmt)
+    if redraw:
+        k = 1
+        while bool((v == 0).any()):
+            alt = g.to_format(g.normal(seed, stream + 64 * k, r * n, n), fmt)
+            v = torch.where(v == 0, alt, v)
+            k += 1
+    return v.view(torch.int32 if fmt == "tf32" else torch.int16).numpy().view(np.uint32 if fmt == "tf32" else np.uint16)
+
+
+def _counter_row_int8(seed, stream, r, n):
+    import tcxgen as g
+    z = g.splitmix(seed, stream, torch.arange(r * n, (r + 1) * n, dtype=torch.int64))
+    return (g._srl(z, 56) - 128).to(torch.int8).numpy()
+
+
+def _counter_row_int32(seed, stream, r, n, lo=-(1 << 20), hi=1 << 20):
+    import tcxgen as g
+    z = g.splitmix(seed, stream, torch.arange(r * n, (r + 1) * n, dtype=torch.int64))
+    return (torch.remainder(g._srl(z, 32), hi - lo + 1) + lo).to(torch.int32).numpy()
+
+
+def _counter_meta_row(seed, r, K):
+    import tcxgen as g
+    G = K // 4
+    z = g.splitmix(seed, g.STREAM_POS, torch.arange(r * G, (r + 1) * G, dtype=torch.int64))
+    pairs = torch.remainder(g._srl(z, 32), 6).to(torch.uint8).view(1, G)
+    return g.sp24_canonical_meta(pairs)[0].numpy().view(np.uint32)
+
+
+# ----------------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="tcx", choices=["tcx", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c3", "c3tf32", "c4", "c5", "c1"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rule)")
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg_names = {"c3": "dense BF16 GEMM M=N=K=8192 (configs[2])", "c3tf32": "dense TF32 GEMM M=N=K=8192 (configs[2])",
+                 "c4": "INT8 GEMM M=N=K=16384 (configs[3])", "c5": "2:4 sparse FP16 GEMM M=65536 N=K=16384 (configs[4])",
+                 "c1": "4096 m16n8k16 FP16 tiles (configs[0])"}
+    metric = "dense & 2:4-sparse MMA TFLOP/s (INT8 TOPS) per B200, % of tensor-core peak"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cb = oracle_sample(args.config, seconds=10.0)
+        line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": cb["unit"], "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": {"c4": "s8", "c3tf32": "tf32", "c5": "f16"}.get(args.config, "bf16"),
+                "data": "synthetic (seeded SplitMix64 / Box-Muller, tcxgen)",
+                "config": {"workload": cfg_names[args.config]},
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    dist_on = world > 1
+    if dist_on:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2206_02874_b200 as tcx
+    tcx.lib()
+    pk = peaks()
+
+    work = Work(args.config, rank, world, dev)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    ms, launches, t0, t1 = time_steps(work, args.steps, args.warmup, dist_on)
+    sampler.stop()
+    clocks = sampler.summary(t0, t1)
+    if dist_on:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    total_flops = work.flops * world
+    total_bytes = work.alg_bytes * world
+    value = (total_bytes / (ms * 1e-3) / 1e9) if work.unit == "GB/s" else total_flops / (ms * 1e-3) / 1e12
+
+    e2e = None
+    if not args.no_e2e:
+        e2e_ms = time_e2e(work, max(3, min(args.steps, 10)), 2)
+        if dist_on:
+            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        ev = (total_bytes / (e2e_ms * 1e-3) / 1e9) if work.unit == "GB/s" else total_flops / (e2e_ms * 1e-3) / 1e12
+        e2e = {"value": round(ev, 3), "unit": work.unit, "h2d_bytes_per_step": work.h2d * world,
+               "d2h_bytes_per_step": work.d2h * world, "ms_per_step": round(e2e_ms, 4)}
+
+    line = {"metric": metric, "value": round(value, 3), "unit": work.unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None,
+            "dtype": {"c3": "bf16", "c3tf32": "tf32", "c4": "s8", "c5": "f16", "c1": "f16"}[args.config],
+            "data": "synthetic (seeded SplitMix64 / Box-Muller, tcxgen; generated on device)",
+            "config": {"workload": cfg_names[args.config], "shape": list(work.shape),
+                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs+outputs per step > 126 MiB L2 (no reuse across steps)" if args.config != "c1"
+                       else "64 rotating batch copies (470 MB) > L2"},
+            "roofline": roofline(work, ms, pk), "clocks": clocks, "gpu_launches": launches,
+            "e2e": e2e}
+    if rank == 0 and world == 1 and not args.no_extras and args.config == "c3":
+        also = {}
+        for extra in ("c3tf32", "c4", "c5", "c1"):
+            try:
+                w2 = Work(extra, 0, 1, dev)
+                ms2, l2, _, _ = time_steps(w2, max(5, min(args.steps, 20)), 3, False)
+                v2 = w2.metric_value(ms2 * 1e-3)
+                also[extra] = {"workload": cfg_names[extra], "value": round(v2, 3), "unit": w2.unit,
+                               "ms_per_step": round(ms2, 5), "roofline": roofline(w2, ms2, pk), "gpu_launches": l2}
+                del w2
+                torch.cuda.empty_cache()
+            except Exception as e:  # report, never hide
+                also[extra] = {"error": f"{type(e).__name__}: {e}"}
+        line["also"] = also
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = oracle_sample(args.config, seconds=10.0)
+        line["cpu_baseline"] = {k: (round(cb[k], 6) if isinstance(cb[k], float) else cb[k])
+                                for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist_on:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

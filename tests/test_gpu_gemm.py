@@ -152,5 +152,5 @@ def test_config4_full_size_int8_bit_exact():
     for _ in range(8):
         r = torch.randint(0, 128, (N, 1), device=DEV, generator=g).double()
         lhs = (Dd @ r).long()
-        rhs = (Ad @ (Bd @ r) + Cd @ r).long()
+        rhs = (Ad @ (Bd.T @ r) + Cd @ r).long()   # D = A B^T (B stored N x K)
         assert torch.equal((lhs - rhs) & 0xFFFFFFFF, torch.zeros_like(lhs))
