@@ -130,6 +130,10 @@ tcx_status tcx_gemm_sp24(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64
                          const void* A_vals, int64_t lda_vals, const void* meta_hw,
                          const void* B, int64_t ldb, const void* C, int64_t ldc,
                          void* D, int64_t ldd, void* stream);
+tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
+                            const void* A_vals, int64_t lda_vals, const void* meta_hw,
+                            const void* B, int64_t ldb, const void* C, int64_t ldc,
+                            void* D, int64_t ldd, const tcx_gemm_opts* opts, void* stream);
 
 /* tcx_round_tf32: out[i] = FP32 -> TF32 round-to-nearest-even of in[i] (low 13 bits
  * cleared; NaN/Inf unchanged; a carry out of max-finite becomes Inf).  in may equal out. */

@@ -29,7 +29,8 @@ _STATUS = {0: "TCX_OK", 1: "TCX_ERR_INVALID_VALUE", 2: "TCX_ERR_UNSUPPORTED", 3:
            4: "TCX_ERR_BAD_SPARSITY", 5: "TCX_ERR_NO_DEVICE", 6: "TCX_ERR_ARCH", 7: "TCX_ERR_CUDA"}
 
 EXPORTS = ["tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
-           "tcx_sp24_meta_hw_bytes", "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_round_tf32", "tcx_probe",
+           "tcx_sp24_meta_hw_bytes", "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_gemm_sp24_ex", "tcx_round_tf32",
+           "tcx_probe",
            "tcx_status_string", "tcx_last_error", "tcx_version", "tcx_launch_count"]
 
 
@@ -76,6 +77,8 @@ def lib():
     L.tcx_sp24_meta_hw_bytes.restype = ctypes.c_size_t
     L.tcx_sp24_pack_meta.argtypes = [i32, i64, i64, vp, vp, vp, vp]
     L.tcx_gemm_sp24.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, vp, i64, vp, i64, vp, i64, vp]
+    L.tcx_gemm_sp24_ex.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, vp, i64, vp, i64, vp, i64,
+                                   ctypes.POINTER(GemmOpts), vp]
     L.tcx_round_tf32.argtypes = [vp, vp, i64, vp]
     L.tcx_probe.argtypes = [i32, ctypes.POINTER(ProbeConfig), ctypes.POINTER(ProbeResult)]
     L.tcx_status_string.restype = ctypes.c_char_p
@@ -83,7 +86,7 @@ def lib():
     L.tcx_version.restype = ctypes.c_char_p
     L.tcx_launch_count.restype = ctypes.c_uint64
     for f in ("tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
-              "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_round_tf32", "tcx_probe"):
+              "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_gemm_sp24_ex", "tcx_round_tf32", "tcx_probe"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -195,7 +198,7 @@ def sp24_pack_meta(meta_canon, M, K, ab=F16, check=True):
     return hw
 
 
-def gemm_sp24(vals, meta_hw, B, C=None, D=None):
+def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0):
     """D = expand(vals, meta) x B + C; vals (M, K/2), B (N, K)."""
     _dev_check(vals, meta_hw, B, C, D)
     ab = ab_code(vals)
@@ -203,8 +206,10 @@ def gemm_sp24(vals, meta_hw, B, C=None, D=None):
     N, K = B.shape
     if D is None:
         D = torch.empty((M, N), dtype=torch.float32, device=vals.device)
-    _check(lib().tcx_gemm_sp24(ab, F32, M, N, K, _ptr(vals), vals.stride(0), _ptr(meta_hw), _ptr(B), B.stride(0),
-                               _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0), _stream(vals)))
+    opts = GemmOpts(cta_group, max_ctas)
+    _check(lib().tcx_gemm_sp24_ex(ab, F32, M, N, K, _ptr(vals), vals.stride(0), _ptr(meta_hw), _ptr(B), B.stride(0),
+                                  _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
+                                  ctypes.byref(opts), _stream(vals)))
     return D
 
 

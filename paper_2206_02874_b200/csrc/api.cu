@@ -229,6 +229,12 @@ tcx_status tcx_sp24_pack_meta(tcx_dtype ab, int64_t M, int64_t K, const uint32_t
 tcx_status tcx_gemm_sp24(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K, const void* A_vals,
                          int64_t lda_vals, const void* meta_hw, const void* B, int64_t ldb, const void* C, int64_t ldc,
                          void* D, int64_t ldd, void* stream) {
+  return tcx_gemm_sp24_ex(ab, cd, M, N, K, A_vals, lda_vals, meta_hw, B, ldb, C, ldc, D, ldd, nullptr, stream);
+}
+
+tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K, const void* A_vals,
+                            int64_t lda_vals, const void* meta_hw, const void* B, int64_t ldb, const void* C,
+                            int64_t ldc, void* D, int64_t ldd, const tcx_gemm_opts* opts, void* stream) {
   if (!((ab == TCX_F16 || ab == TCX_BF16) && cd == TCX_F32))
     return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: (ab=%d, cd=%d) not supported (NEXT: bf16/i8/tf32 variants)", ab, cd);
   if (M < 0 || N < 0 || K < 0) return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm_sp24: negative size");
@@ -242,6 +248,12 @@ tcx_status tcx_gemm_sp24(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64
   st = current_device(&dev);
   if (st != TCX_OK) return st;
   GemmArgs g{ab, M, N, K, A_vals, lda_vals, B, ldb, C, ldc, D, ldd, meta_hw, 2, 0};
+  if (opts) {
+    if (opts->cta_group == 1 || opts->cta_group == 2) g.cta_group = opts->cta_group;
+    g.max_ctas = opts->max_ctas;
+  }
+  if (g.cta_group == 2 && M % 256)
+    return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: the CTA-pair kernel needs M %% 256 == 0 (use cta_group=1)");
   return launch_gemm_sp24(g, dev, (cudaStream_t)stream);
 }
 

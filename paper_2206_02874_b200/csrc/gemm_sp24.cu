@@ -1,7 +1,265 @@
-// tcx 2:4 sparse GEMM (tcgen05.mma.sp) — built in the next step.
+// tcx 2:4 structured-sparse GEMM on sm_100a (the paper's mma.sp, at GEMM scale):
+//     D = expand(sA, e) x B + C
+// sA: M x K/2 kept values (K-major), e: hardware metadata image (sp24.cu), B: N x K, C/D: M x N FP32.
+//
+// Same warp-specialised persistent structure as gemm_dense.cu; per 128-logical-K stage each CTA
+// TMA-loads 128 rows of sA (128 B/row, SW128), its half of the B tile (two SW128 64-element
+// boxes) and one 2 KiB metadata atom; the MMA thread copies the atom smem -> TMEM with
+// tcgen05.cp 128x128b, then issues 4 x tcgen05.mma.sp.kind::f16 (logical K = 32 each).
+// TMEM: two 240-column FP32 accumulators (cols 0 and 256) + a 4-slot metadata ring (cols 496..511),
+// so the epilogue of tile t overlaps the MMAs of tile t+1 (UMMA N = 240: 2 x 240 + 16 <= 512).
+// "The hardware selector determines which values should participate ... on the fly":
+// the MMA skips the zero products; throughput doubles at the same latency.
 #include "tcx_internal.h"
+#include "ptx.cuh"
+
 namespace tcx {
-tcx_status launch_gemm_sp24(const GemmArgs&, const DevInfo&, cudaStream_t) {
-  return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: not built yet");
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 240;            // UMMA N
+constexpr int ACC_STRIDE = 256;    // TMEM column offset between the two accumulators
+constexpr int META_COL = 496;      // metadata ring: 4 slots x 4 columns
+constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARPS = 4;
+constexpr int GROUP_M = 8;
+constexpr int KL = 128;            // logical K per stage
+constexpr int META_BYTES = 2048;   // one 128-row x 128-logical-K metadata atom
+
+template <int CG>
+struct SpCfg {
+  static constexpr int BN_LOAD = BN / CG;
+  static constexpr int A_BYTES = BM * 128;                 // 64 kept fp16 per row
+  static constexpr int B_HALF = BN_LOAD * 128;             // one 64-element SW128 box
+  static constexpr int B_BYTES = 2 * B_HALF;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + META_BYTES;
+  static constexpr int STAGES = CG == 1 ? 2 : 4;
+  static constexpr int SMEM_DATA = STAGES * STAGE_BYTES;
+  static constexpr int SMEM_TOTAL = SMEM_DATA + 1024 + 1024;
+  static_assert(B_HALF % 1024 == 0, "SW128 atoms need 1 KiB alignment");
+};
+
+struct Smem {
+  uint64_t full[8];
+  uint64_t empty[8];
+  uint64_t tmem_full[2];
+  uint64_t tmem_empty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64_t n_tiles, int64_t& mt, int64_t& nt) {
+  int64_t per_group = (int64_t)GROUP_M * n_tiles;
+  int64_t g = tile / per_group;
+  int64_t first_m = g * GROUP_M;
+  int64_t gm = m_tiles - first_m < GROUP_M ? m_tiles - first_m : GROUP_M;
+  int64_t r = tile - g * per_group;
+  mt = first_m + r % gm;
+  nt = r / gm;
 }
+
+template <int CG>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmE, int64_t M, int64_t N, int64_t K,
+                 const float* __restrict__ Cptr, int64_t ldc, float* __restrict__ Dptr, int64_t ldd, uint32_t idesc) {
+  using C_ = SpCfg<CG>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  Smem* sm = (Smem*)(smem + C_::SMEM_DATA);
+
+  const int warp = threadIdx.x / 32;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int64_t m_tiles = M / (BM * CG);
+  const int64_t n_tiles = (N + BN - 1) / BN;
+  const int64_t num_tiles = m_tiles * n_tiles;
+  const int64_t k_blocks = K / KL;
+  const int64_t cluster_id = blockIdx.x / CG;
+  const int64_t num_clusters = gridDim.x / CG;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C_::STAGES; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&sm->tmem_full[a], 1); mbar_init(&sm->tmem_empty[a], EPI_WARPS * CG); }
+    fence_mbar_init();
+  }
+  if (warp == 0 && elect_one()) { tma_prefetch(&tmA); tma_prefetch(&tmB); tma_prefetch(&tmE); }
+  if (warp == 2) { tmem_alloc<CG>(&sm->tmem_base, 512); tmem_relinquish<CG>(); }
+  tc05_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  tc05_fence_after();
+  const uint32_t tmem_base = sm->tmem_base;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0; uint32_t phase = 0;
+      const uint32_t full0_cluster = CG == 2 ? mapa(smem_u32(&sm->full[0]), 0) : 0;
+      for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        int64_t mt, nt;
+        tile_coords(tile, m_tiles, n_tiles, mt, nt);
+        const int64_t mrow = mt * BM * CG + rank * BM;
+        const int brow = (int)(nt * BN + rank * C_::BN_LOAD);
+        const int64_t mb = mrow / 128;
+        for (int64_t kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&sm->empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C_::STAGE_BYTES;
+          uint8_t* sb = sa + C_::A_BYTES;
+          uint8_t* se = sb + C_::B_BYTES;
+          const int ka = (int)(kb * 64);           // kept-value column
+          const int kx = (int)(kb * KL);           // logical column of B
+          const int erow = (int)((mb * k_blocks + kb) * 16);
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(&sm->full[stage], C_::STAGE_BYTES);
+            tma_load_2d(sa, &tmA, &sm->full[stage], ka, (int)mrow);
+            tma_load_2d(sb, &tmB, &sm->full[stage], kx, brow);
+            tma_load_2d(sb + C_::B_HALF, &tmB, &sm->full[stage], kx + 64, brow);
+            tma_load_2d(se, &tmE, &sm->full[stage], 0, erow);
+          } else {
+            if (leader) mbar_arrive_expect_tx(&sm->full[stage], 2 * C_::STAGE_BYTES);
+            const uint32_t bar = full0_cluster + stage * 8;
+            tma_load_2d_cg2(sa, &tmA, bar, ka, (int)mrow);
+            tma_load_2d_cg2(sb, &tmB, bar, kx, brow);
+            tma_load_2d_cg2(sb + C_::B_HALF, &tmB, bar, kx + 64, brow);
+            tma_load_2d_cg2(se, &tmE, bar, 0, erow);
+          }
+          if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t acc_phase = 0;
+      for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        if constexpr (CG == 2) mbar_wait_cluster(&sm->tmem_empty[acc], acc_phase ^ 1);
+        else mbar_wait(&sm->tmem_empty[acc], acc_phase ^ 1);
+        tc05_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * ACC_STRIDE;
+        for (int64_t kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&sm->full[stage], phase);
+          tc05_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = smem_u32(smem + stage * C_::STAGE_BYTES);
+            const uint32_t sb = sa + C_::A_BYTES;
+            const uint32_t se = sb + C_::B_BYTES;
+            const uint32_t tmeta = tmem_base + META_COL + stage * 4;
+            // metadata atom -> TMEM (128 lanes x 16 B); executes in order before the MMAs below
+            tc05_cp_128x128b<CG>(tmeta, sdesc(se, 128, 128, 0));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint64_t ad = sdesc(sa + j * 32, 16, 1024, 2);
+              const uint64_t bd = sdesc(sb + (j >> 1) * C_::B_HALF + (j & 1) * 64, 16, 1024, 2);
+              const uint32_t e = tmeta + j;
+              umma_sp<CG, KIND_F16>(tmem_d, ad, bd, e & ~1u, idesc | (e & 1u), (kb | j) ? 1u : 0u);
+            }
+            tc05_commit<CG>(&sm->empty[stage]);
+            if (kb == k_blocks - 1) tc05_commit<CG>(&sm->tmem_full[acc]);
+          }
+          __syncwarp();
+          if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int e = warp - 4;
+    const int lane = threadIdx.x & 31;
+    int acc = 0; uint32_t acc_phase = 0;
+    const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), 0) : smem_u32(&sm->tmem_empty[0]);
+    for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+      int64_t mt, nt;
+      tile_coords(tile, m_tiles, n_tiles, mt, nt);
+      const int64_t row = mt * BM * CG + rank * BM + e * 32 + lane;
+      const int64_t col0 = nt * BN;
+      mbar_wait(&sm->tmem_full[acc], acc_phase);
+      tc05_fence_after();
+      constexpr int NCH = BN / 16;
+#pragma unroll 1
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int64_t c0 = col0 + ch * 16;
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(tmem_base + acc * ACC_STRIDE + ch * 16 + ((uint32_t)(e * 32) << 16), v);
+        uint32_t cv[16];
+        const bool ok = c0 < N;          // N % 16 == 0: a chunk is all-in or all-out
+        if (Cptr != nullptr && ok) {
+          const uint4* crow = (const uint4*)(Cptr + row * ldc + c0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 t = __ldg(crow + j);
+            cv[4 * j] = t.x; cv[4 * j + 1] = t.y; cv[4 * j + 2] = t.z; cv[4 * j + 3] = t.w;
+          }
+        }
+        tmem_ld_wait();
+        if (ch == NCH - 1) {
+          tc05_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tmem_empty_cluster + acc * 8);
+        }
+        if (ok) {
+          uint4* drow = (uint4*)(Dptr + row * ldd + c0);
+          if (Cptr != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__fadd_rn(__uint_as_float(v[j]), __uint_as_float(cv[j])));
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) drow[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc05_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if (warp == 2) { tc05_fence_after(); tmem_dealloc<CG>(tmem_base, 512); }
+}
+
+template <int CG>
+tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
+  using C_ = SpCfg<CG>;
+  if (a.M % (BM * CG)) return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: M %% %d != 0", BM * CG);
+  const CUtensorMapDataType dt = a.ab == TCX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tA, tB, tE;
+  tcx_status st = make_tmap_2d(&tA, dt, a.A, (uint64_t)(a.K / 2), (uint64_t)a.M, (uint64_t)(a.lda * 2), 64, BM,
+                               CU_TENSOR_MAP_SWIZZLE_128B);
+  if (st != TCX_OK) return st;
+  st = make_tmap_2d(&tB, dt, a.B, (uint64_t)a.K, (uint64_t)a.N, (uint64_t)(a.ldb * 2), 64, C_::BN_LOAD,
+                    CU_TENSOR_MAP_SWIZZLE_128B);
+  if (st != TCX_OK) return st;
+  const uint64_t meta_rows = (uint64_t)(a.M * a.K / 8) / 128;
+  st = make_tmap_2d(&tE, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.meta_hw, 128, meta_rows, 128, 128, 16,
+                    CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (st != TCX_OK) return st;
+  auto kern = gemm_sp24_kernel<CG>;
+  TCX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_TOTAL));
+  const int64_t tiles = (a.M / (BM * CG)) * ((a.N + BN - 1) / BN);
+  int64_t clusters = tiles;
+  int64_t max_clusters = dev.sm_count / CG;
+  if (a.max_ctas > 0 && a.max_ctas / CG < max_clusters) max_clusters = a.max_ctas / CG > 0 ? a.max_ctas / CG : 1;
+  if (clusters > max_clusters) clusters = max_clusters;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(clusters * CG));
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C_::SMEM_TOTAL;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr; cfg.numAttrs = 1;
+  // idesc: sparse flag [2], c F32 [4,6)=1, a/b format [7,10)/[10,13), N>>3 [17,23), M>>4 [24,29)
+  const uint32_t fmt = a.ab == TCX_BF16 ? 1u : 0u;
+  const uint32_t idesc = (1u << 2) | (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
+                         ((uint32_t)((BM * CG) >> 4) << 24);
+  TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tE, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K, (const float*)a.C,
+                                  (int64_t)a.ldc, (float*)a.D, (int64_t)a.ldd, idesc));
+  count_launch();
+  return TCX_OK;
+}
+
+}  // namespace
+
+tcx_status launch_gemm_sp24(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
+  if (a.cta_group == 1) return launch_sp<1>(a, dev, s);
+  return launch_sp<2>(a, dev, s);
+}
+
 }  // namespace tcx
