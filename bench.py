@@ -155,8 +155,8 @@ class Work:
             self.kernel = "gemm_dense_kernel<2,2>"
             self.step = lambda: tcx.gemm(self.A, self.B, self.C, self.D)
             self.unit, self.bound = "TOPS", "tensor"
-        elif cfg == "c5":
-            M, N, K = 65536, 16384, 16384
+        elif cfg in ("c5", "c5s"):       # c5s: an 8192-row slice of C5 (profiling only)
+            M, N, K = (65536 if cfg == "c5" else 8192), 16384, 16384
             self.kind = "sp16"
             self.shape = (M, N, K)
             m0, m1 = self._rows(M)
@@ -169,7 +169,9 @@ class Work:
             self.B = self._bcast(lambda: g.normal_matrix((N, K), "f16", seed, g.STREAM_B, dev))
             self.C = torch.zeros(m1 - m0, N, dtype=torch.float32, device=dev)
             self.D = torch.empty(m1 - m0, N, dtype=torch.float32, device=dev)
-            self.flops = 2.0 * (m1 - m0) * N * K / 2          # effective (kept products); dense-eq = 2x
+            # dense-equivalent FLOPs 2MNK (NVIDIA's sparse convention: peak = 2x dense); the effective
+            # (kept-product) rate is half of it and is reported beside it (DESIGN.md R-C13)
+            self.flops = 2.0 * (m1 - m0) * N * K
             self.alg_bytes = self.vals.numel() * 2 + self.meta_hw.numel() + self.B.numel() * 2 + 8 * (m1 - m0) * N
             self.kernel = "gemm_sp24_kernel"
             self.step = lambda: tcx.gemm_sp24(self.vals, self.meta_hw, self.B, self.C, self.D)
@@ -183,16 +185,25 @@ class Work:
             self.Bs = [g.uniform_matrix((count, 8, 16), "f16", seed + i, g.STREAM_B, device=dev) for i in range(copies)]
             self.Cs = [g.uniform_matrix((count, 16, 8), "f32", seed + i, g.STREAM_C, device=dev) for i in range(copies)]
             self.Ds = [torch.empty(count, 16, 8, device=dev) for _ in range(copies)]
-            self.i = 0
-            self.flops = 4096.0 * count
-            self.alg_bytes = 1792 * count
+            # one step = one CUDA-graph replay of 64 tcx_mma_tiles calls over the 64 copies (the
+            # kernel is ~2 us; the graph removes host launch overhead from the device timing)
+            self.flops = 4096.0 * count * copies
+            self.alg_bytes = 1792 * count * copies
             self.kernel = "tiles16_kernel<0>"
-
-            def step():
-                j = self.i % copies
-                self.i += 1
-                tcx.mma_tiles(self.As[j], self.Bs[j], self.Cs[j], self.Ds[j])
-            self.step = step
+            self.launches_per_step = copies
+            torch.cuda.synchronize()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                for j in range(copies):            # warm (module load) outside capture
+                    tcx.mma_tiles(self.As[j], self.Bs[j], self.Cs[j], self.Ds[j])
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                for j in range(copies):
+                    tcx.mma_tiles(self.As[j], self.Bs[j], self.Cs[j], self.Ds[j])
+            self.step = self.graph.replay
             self.unit, self.bound = "GB/s", "hbm"
         else:
             raise ValueError(cfg)
@@ -273,7 +284,7 @@ def time_steps(work, steps, warmup, dist_on, sampler=None):
     t1 = time.time()
     if dist_on:
         torch.distributed.barrier()
-    launches = tcx.launch_count() - n0
+    launches = tcx.launch_count() - n0 + steps * getattr(work, "launches_per_step", 0)   # graph replays launch without the host counter
     return e0.elapsed_time(e1) / steps, launches, t0, t1
 
 
