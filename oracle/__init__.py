@@ -63,6 +63,8 @@ def lib():
         L.tcxref_tiles.argtypes = [i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]; L.tcxref_tiles.restype = i32
         L.tcxref_model_dot.argtypes = [i32, i32, vp, vp, u32, i32, i32, i32, i32, i32, i32]
         L.tcxref_model_dot.restype = u32
+        L.tcxref_model_batch.argtypes = [i32, ctypes.c_long, i32, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, i32]
+        L.tcxref_model_batch.restype = i32
         L.tcxref_seq32.argtypes = [i32, vp, vp, ctypes.c_float, i32]; L.tcxref_seq32.restype = ctypes.c_float
         _lib = L
     return _lib
@@ -186,3 +188,18 @@ def model_dot(ab: int, a_bits, b_bits, c_bits: int, Ki: int, g: int, p: int, rz:
 def seq32(a: np.ndarray, b: np.ndarray, c: float, c_last: bool = False) -> float:
     a = _c(a, np.float32); b = _c(b, np.float32)
     return float(lib().tcxref_seq32(a.size, _p(a), _p(b), float(c), int(c_last)))
+
+
+def model_batch(ab: int, a_rows, b_rows, c_bits, Ki: int, g: int, p: int, rz: bool, floor_mode=False,
+                c_after=False, emode=0, nthreads=None) -> np.ndarray:
+    """model_dot over n rows at once (n x K element bits for a and b, n FP32 bits for c).
+    emode 0: align on the actual leading bit of the largest addend; 1: on exponent sums
+    (product nominal leading exponent = e_a + e_b + 1, subnormal inputs at emin)."""
+    a = _c(a_rows, _NP[ab]); b = _c(b_rows, _NP[ab]); c = _c(c_bits, np.uint32)
+    n, K = a.shape
+    out = np.zeros(n, dtype=np.uint32)
+    nt = nthreads or len(os.sched_getaffinity(0))
+    rc = lib().tcxref_model_batch(ab, n, K, _p(a), _p(b), _p(c), Ki, g, p, int(rz), int(floor_mode), int(c_after),
+                                  int(emode), _p(out), nt)
+    assert rc == 0
+    return out

@@ -35,10 +35,15 @@ enum { REF_F16 = 0, REF_BF16 = 1, REF_TF32 = 2, REF_F32 = 3 };
 uint32_t tcxref_sum_round(int n, const int *signs, const uint64_t *mants, const int *exps,
                           int out_fmt, int rz);
 
-typedef struct { int zero; int sign; uint64_t mant; int exp; } term;
+typedef struct { int zero; int sign; uint64_t mant; int exp; int eu; int nlead; } term;
+/* eu: unbiased exponent of an input (emin for subnormals); 1000 marks the accumulator term.
+   nlead: 'nominal' leading-bit exponent used by the exponent-sum alignment variants:
+   emode 1: product = eu_a + eu_b + 1 (a product of two [1,2) significands lies in [1,4)),
+            accumulator / c = its actual leading bit;
+   emode 2: as 1, but the accumulator / c is also placed in the 2-integer-bit frame (lead + 1). */
 
 static term dec(int fmt, uint32_t b) {
-  term t = {1, 0, 0, 0};
+  term t = {1, 0, 0, 0, 0, 0};
   int ebits, fbits, bias;
   uint32_t e, f;
   if (fmt == REF_F16) { ebits = 5; fbits = 10; bias = 15; b &= 0xFFFF; }
@@ -47,6 +52,7 @@ static term dec(int fmt, uint32_t b) {
   t.sign = (b >> (ebits + fbits)) & 1;
   e = (b >> fbits) & ((1u << ebits) - 1);
   f = b & ((1u << fbits) - 1);
+  t.eu = e == 0 ? 1 - bias : (int)e - bias;
   if (e == 0 && f == 0) return t;
   t.zero = 0;
   if (e == 0) { t.mant = f; t.exp = 1 - bias - fbits; }
@@ -81,20 +87,30 @@ static uint32_t sum_terms(int n, const term *ts, int rz) {
   return tcxref_sum_round(k, s, m, e, REF_F32, rz);
 }
 
-static term from_f32(uint32_t b) { return dec(REF_F32, b); }
+static term from_f32(uint32_t b) {
+  term t = dec(REF_F32, b);
+  if (!t.zero) t.nlead = lead_exp(t);
+  t.eu = 1000;                                               /* marks the accumulator term */
+  return t;
+}
 
 /* align + truncate a set of terms relative to their largest addend */
-static void align_trunc(int n, term *ts, int p, int floor_mode) {
+static void align_trunc(int n, term *ts, int p, int floor_mode, int emode) {
   int i, emax = -100000, L;
   if (p < 0) return;
-  for (i = 0; i < n; i++) if (!ts[i].zero) { int le = lead_exp(ts[i]); if (le > emax) emax = le; }
+  for (i = 0; i < n; i++)
+    if (!ts[i].zero) {
+      int le = emode ? ts[i].nlead : lead_exp(ts[i]);
+      if (emode == 2 && ts[i].eu == 1000) le += 1;          /* accumulator / c: 2-integer-bit format */
+      if (le > emax) emax = le;
+    }
   if (emax == -100000) return;
   L = emax - 23 - p;
   for (i = 0; i < n; i++) ts[i] = trunc_to(ts[i], L, floor_mode);
 }
 
-uint32_t tcxref_model_dot(int ab, int K, const void *a, const void *b, uint32_t c_bits,
-                          int Ki, int g, int p, int rz, int floor_mode, int c_after) {
+uint32_t tcxref_model_dot2(int ab, int K, const void *a, const void *b, uint32_t c_bits,
+                           int Ki, int g, int p, int rz, int floor_mode, int c_after, int emode) {
   uint32_t acc = c_bits;
   int k0, j;
   for (k0 = 0; k0 < K; k0 += Ki) {           /* one instruction */
@@ -110,9 +126,10 @@ uint32_t tcxref_model_dot(int ab, int K, const void *a, const void *b, uint32_t 
         term x = dec(ab, ab_bits), y = dec(ab, bb_bits), pr;
         pr.zero = x.zero || y.zero; pr.sign = x.sign ^ y.sign;
         pr.mant = pr.zero ? 0 : x.mant * y.mant; pr.exp = x.exp + y.exp;
+        pr.eu = 0; pr.nlead = x.eu + y.eu + 1;
         ts[n++] = pr;
       }
-      align_trunc(n, ts, p, floor_mode);
+      align_trunc(n, ts, p, floor_mode, emode);
       if (!c_after) {
         acc = sum_terms(n, ts, rz);
       } else {
@@ -127,6 +144,11 @@ uint32_t tcxref_model_dot(int ab, int K, const void *a, const void *b, uint32_t 
   return acc;
 }
 
+uint32_t tcxref_model_dot(int ab, int K, const void *a, const void *b, uint32_t c_bits,
+                          int Ki, int g, int p, int rz, int floor_mode, int c_after) {
+  return tcxref_model_dot2(ab, K, a, b, c_bits, Ki, g, p, rz, floor_mode, c_after, 0);
+}
+
 /* the paper's CPU FP32 baseline: sequential binary32 (no FMA contraction; built with
    -ffp-contract=off), ascending k, c first (c_last=0) or last (c_last=1). */
 float tcxref_seq32(int K, const float *a, const float *b, float c, int c_last) {
@@ -138,4 +160,40 @@ float tcxref_seq32(int K, const float *a, const float *b, float c, int c_last) {
   }
   if (c_last) acc = acc + c;
   return acc;
+}
+
+/* batched model evaluation over n dot products (rows of a and b: n x K element bits), threaded. */
+#include <pthread.h>
+typedef struct {
+  int ab, K; const void *a, *b; const uint32_t *c; int Ki, g, p, rz, floor_mode, c_after, emode;
+  uint32_t *out; long s0, s1;
+} mjob;
+
+static void *mworker(void *arg) {
+  mjob *j = (mjob *)arg;
+  long i;
+  size_t es = (j->ab == REF_F16 || j->ab == REF_BF16) ? 2 : 4;
+  for (i = j->s0; i < j->s1; i++)
+    j->out[i] = tcxref_model_dot2(j->ab, j->K, (const char *)j->a + (size_t)i * j->K * es,
+                                  (const char *)j->b + (size_t)i * j->K * es, j->c[i], j->Ki, j->g, j->p,
+                                  j->rz, j->floor_mode, j->c_after, j->emode);
+  return NULL;
+}
+
+int tcxref_model_batch(int ab, long n, int K, const void *a, const void *b, const uint32_t *c, int Ki, int g,
+                       int p, int rz, int floor_mode, int c_after, int emode, uint32_t *out, int nthreads) {
+  pthread_t th[256];
+  mjob jobs[256];
+  int t;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  for (t = 0; t < nthreads; t++) {
+    mjob *j = &jobs[t];
+    j->ab = ab; j->K = K; j->a = a; j->b = b; j->c = c; j->Ki = Ki; j->g = g; j->p = p; j->rz = rz;
+    j->floor_mode = floor_mode; j->c_after = c_after; j->emode = emode; j->out = out;
+    j->s0 = n * t / nthreads; j->s1 = n * (t + 1) / nthreads;
+    if (pthread_create(&th[t], NULL, mworker, j)) return -1;
+  }
+  for (t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+  return 0;
 }

@@ -200,3 +200,140 @@ def sp24_problem(M, K, seed, fmt="f16", device="cpu"):
     pairs = sp24_pairs(M, K, seed, STREAM_POS, device)
     vals = normal_matrix((M, K // 2), fmt, seed, STREAM_SPVAL, device, redraw_zero=True)
     return vals, sp24_canonical_meta(pairs)
+
+
+# ----------------------------------------------------------------------------------------------
+# Config 2: crafted numeric-probe tiles (SURVEY §8(d) "The eight C2 crafted classes").
+# Each tile is m16n8k16 (TF32: k16 = two chained k8); only d00 is probed, the paper's placement
+# (PAPER.md:900): values in row 0 of A, column 0 of B ("n-row" 0 of the stored B) and c00,
+# everything else zero.  Random numbers only; the MMA arithmetic lives elsewhere.
+# ----------------------------------------------------------------------------------------------
+CLASSES = ("SPREAD", "CANCEL", "BIGC", "LADDER", "TIES", "SUBNORMAL", "PAPER3_init_low", "PAPER3_init_FP32")
+PROBE_TYPES = ("mul", "inner", "accum", "accum_c32")
+
+
+def _u(seed, stream, n, k=1):
+    return uniform01(seed, stream, 0, n * k).view(n, k).double()
+
+
+def probe_classes(fmt, n_per_class=8192, seed=0):
+    """returns dict: A (T,16,16), B (T,8,16), C (T,16,8) [stored formats], cls (T,), ptype (T,),
+    a32/b32/c32 (T,16)/(T,16)/(T,): the FP32 values the paper's CPU baseline would use."""
+    import numpy as np
+    K = 16
+    T = n_per_class * len(CLASSES)
+    a = torch.zeros(T, K, dtype=torch.float64)
+    b = torch.zeros(T, K, dtype=torch.float64)
+    c = torch.zeros(T, dtype=torch.float64)
+    a32 = torch.zeros(T, K, dtype=torch.float64)      # CPU-baseline inputs for PAPER3_init_FP32
+    b32 = torch.zeros(T, K, dtype=torch.float64)
+    c32 = torch.zeros(T, dtype=torch.float64)
+    ptype = torch.full((T,), -1, dtype=torch.int64)
+    cls = torch.arange(T) // n_per_class
+    emin = {"f16": -14, "bf16": -126, "tf32": -126}[fmt]
+    fbits = {"f16": 10, "bf16": 7, "tf32": 10}[fmt]
+    n = n_per_class
+
+    def sig(u):                                        # random significand in [1, 2) with fbits bits
+        return 1.0 + torch.floor(u * (1 << fbits)) / (1 << fbits)
+
+    def sgn(u):
+        return torch.where(u < 0.5, -1.0, 1.0).double()
+
+    def split(e, ua, ub, us):                          # product exponent e -> a, b with normal exponents
+        ea = torch.floor(e / 2.0)
+        eb = e - ea
+        ea = torch.clamp(ea, min=emin)
+        eb = e - ea
+        return sgn(us) * sig(ua) * torch.pow(2.0, ea), sig(ub) * torch.pow(2.0, eb)
+
+    for ci, name in enumerate(CLASSES):
+        s = slice(ci * n, (ci + 1) * n)
+        st = 16 + ci
+        U = _u(seed, st, n, 8 * K)
+        if name == "SPREAD":
+            e = torch.floor(U[:, 0:K] * 41) - 30                  # product exponents in [-30, 10]
+            a[s], b[s] = split(e, U[:, K:2 * K], U[:, 2 * K:3 * K], U[:, 3 * K:4 * K])
+        elif name == "CANCEL":
+            e = torch.floor(U[:, 0:K] * 8) - 4
+            x, y = split(e, U[:, K:2 * K], U[:, 2 * K:3 * K], U[:, 3 * K:4 * K])
+            x[:, 1::2] = -x[:, 0::2]
+            y[:, 1::2] = y[:, 0::2]
+            er = -(10 + torch.floor(U[:, 4 * K] * 21))            # residual 2^-10 .. 2^-30
+            rx, ry = split(er.unsqueeze(1), U[:, 5 * K:5 * K + 1], U[:, 5 * K + 1:5 * K + 2], U[:, 5 * K + 2:5 * K + 3])
+            x[:, 14:15], y[:, 14:15] = rx, ry
+            x[:, 15], y[:, 15] = 0.0, 0.0
+            a[s], b[s] = x, y
+            c[s] = (normal(seed, st + 64, 0, n).double()).to(torch.float32).double()
+        elif name == "BIGC":
+            m = torch.floor(U[:, 6 * K] * (1 << 23))
+            c[s] = sgn(U[:, 6 * K + 1]) * (2.0 ** 24) * (1 + m * 2.0 ** -23)
+            e = torch.floor(U[:, 0:K] * 33) - 30                  # products 2^-30 .. 2^2
+            a[s], b[s] = split(e, U[:, K:2 * K], U[:, 2 * K:3 * K], U[:, 3 * K:4 * K])
+        elif name == "LADDER":
+            j = torch.floor(U[:, 0] * 11)                         # 16 equal products 2^-j, j = 0..10
+            ea = -torch.floor(j / 2)
+            a[s] = torch.pow(2.0, ea).unsqueeze(1).expand(n, K)
+            b[s] = torch.pow(2.0, -j - ea).unsqueeze(1).expand(n, K)
+            c[s] = 2.0 ** 24
+        elif name == "TIES":
+            t = torch.floor(U[:, 0] * (1 << 20))
+            c[s] = sgn(U[:, 1]) * (2.0 ** 24 + 2 * t)             # ulp(c) = 2: a product of +-1 is a tie
+            v = torch.floor(U[:, 2] * 3)
+            x = torch.zeros(n, K, dtype=torch.float64)
+            y = torch.zeros(n, K, dtype=torch.float64)
+            pm = sgn(U[:, 3])
+            x[:, 0] = pm                                          # exact tie
+            y[:, 0] = 1.0
+            sel = v == 1                                          # tie made of two halves
+            x[sel, 0] = pm[sel] * 0.5
+            x[sel, 1] = pm[sel] * 0.5
+            y[sel, 1] = 1.0
+            sel = v == 2                                          # just above/below the tie
+            j = 12 + torch.floor(U[:, 4] * 10)
+            x[sel, 1] = (sgn(U[:, 5]) * torch.pow(2.0, -j))[sel]
+            y[sel, 1] = 1.0
+            a[s], b[s] = x, y
+        elif name == "SUBNORMAL":
+            if fmt == "f16":                                      # FP16 subnormal inputs (2^-24 .. 2^-15)
+                ea = -(15 + torch.floor(U[:, 0:K] * 10))
+                x = sgn(U[:, K:2 * K]) * torch.floor(1 + U[:, 2 * K:3 * K] * 1023) * 2.0 ** -24
+                x = torch.where(U[:, 3 * K:4 * K] < 0.5, x, sgn(U[:, K:2 * K]) * torch.pow(2.0, ea))
+                y = sig(U[:, 4 * K:5 * K]) * torch.pow(2.0, torch.floor(U[:, 5 * K:6 * K] * 20) - 10)
+            else:                                                 # products below 2^-126: FP32-subnormal results
+                e = -(127 + torch.floor(U[:, 0:K] * 22))          # 2^-127 .. 2^-148
+                x, y = split(e, U[:, K:2 * K], U[:, 2 * K:3 * K], U[:, 3 * K:4 * K])
+            a[s], b[s] = x, y
+            c[s] = torch.where(U[:, 7 * K] < 0.5, 0.0, sgn(U[:, 7 * K + 1]) * 2.0 ** -140 * torch.floor(1 + U[:, 7 * K + 2] * 7))
+        else:  # PAPER3: a0b0 / a0b0 + a1b1 / a0b0 + c0 (c0 low-format or FP32), N(0,1), one seed
+            z = normal(seed, 16 + 6, 0, 5 * n).view(n, 5).double()   # the same draws for both inits
+            z32 = z.to(torch.float32).double()
+            pt = torch.arange(n) % 4
+            x = torch.zeros(n, K, dtype=torch.float64)
+            y = torch.zeros(n, K, dtype=torch.float64)
+            cc = torch.zeros(n, dtype=torch.float64)
+            x[:, 0], y[:, 0] = z32[:, 0], z32[:, 1]
+            inner = pt == 1
+            x[inner, 1], y[inner, 1] = z32[inner, 2], z32[inner, 3]
+            acc = pt >= 2
+            cc[acc] = z32[acc, 4]
+            a32[s], b32[s], c32[s] = x, y, cc
+            a[s], b[s] = x, y
+            if name == "PAPER3_init_low":                     # created in low precision: baseline = same values
+                a[s] = to_format(x, fmt).double()
+                b[s] = to_format(y, fmt).double()
+                a32[s], b32[s] = a[s], b[s]
+                clow = torch.where(pt == 2, to_format(cc, fmt).double(), cc)    # accum: c0 low; accum_c32: FP32
+                c[s] = clow
+                c32[s] = clow
+            else:
+                c[s] = cc
+            ptype[s] = pt
+    A = torch.zeros(T, 16, K, dtype=torch.float64)
+    B = torch.zeros(T, 8, K, dtype=torch.float64)
+    A[:, 0, :] = a
+    B[:, 0, :] = b
+    C = torch.zeros(T, 16, 8, dtype=torch.float32)
+    C[:, 0, 0] = c.to(torch.float32)
+    return {"A": to_format(A, fmt), "B": to_format(B, fmt), "C": C, "cls": cls, "ptype": ptype,
+            "a32": a32.to(torch.float32), "b32": b32.to(torch.float32), "c32": c32.to(torch.float32), "K": K}
