@@ -209,17 +209,18 @@ class Work:
             raise ValueError(cfg)
 
     def _rows(self, M):
-        per = M // self.world
-        return self.rank * per, (self.rank + 1) * per
+        from paper_2206_02874_b200.dist import row_shard
+        return row_shard(M, self.world, self.rank)
 
     def _bcast(self, make):
         import torch.distributed as dist
         if self.world == 1:
             return make()
+        from paper_2206_02874_b200.dist import broadcast_replicated
         t = make()               # every rank allocates B; rank 0's copy is the one broadcast
         if self.rank != 0:
             t.zero_()
-        dist.broadcast(t, src=0)
+        broadcast_replicated(t, src=0)    # one-time NCCL broadcast over NVLink (not timed)
         return t
 
     def metric_value(self, seconds_per_step):
