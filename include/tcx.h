@@ -67,9 +67,11 @@ typedef enum { TCX_F16 = 0, TCX_BF16 = 1, TCX_TF32 = 2, TCX_F32 = 3, TCX_S8 = 4,
  *     D_t = A_t x B_t + C_t,   t < count
  * A: count x m x k row-major (ab elements);  B: count x n x k (n-major "col", ab elements);
  * C, D: count x m x n row-major (cd elements).  C == NULL -> zeros.
- * Supported (ab, cd, m, n, k):  (F16|BF16, F32, 16, 8, 16)  (TF32, F32, 16, 8, 8|16)
- *                               (S8, S32, 16, 8, 32).  TF32 k=16 = two chained k=8 MMAs,
- *                               the first's D feeding the second's C (DESIGN.md R-C15).
+ * Supported (ab, cd, m, n, k):  (F16|BF16, F32, 16, 8, 16|8)  (F16, F16, 16, 8, 16|8)
+ *                               (TF32, F32, 16, 8, 8|16)  (S8, S32, 16, 8, 32).
+ *   TF32 k=16 = two chained k=8 MMAs, the first's D feeding the second's C (DESIGN.md R-C15).
+ *   (F16, F16): C and D are FP16 (2-byte elements) — the FP16-accumulate mma variant of Table
+ *   A100-mma whose numerics PAPER.md:962-982 profiles.
  * count == 0 is a no-op.  Others -> TCX_ERR_UNSUPPORTED.
  * ------------------------------------------------------------------------------------- */
 tcx_status tcx_mma_tiles(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, int64_t count,
@@ -90,7 +92,8 @@ tcx_status tcx_gemm(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
 typedef struct {
   int cta_group;   /* 1 or 2 (CTA pair, tcgen05 cta_group::2) */
   int max_ctas;    /* cap on persistent CTAs (0 = all SMs) */
-  int reserved[6];
+  int group_m;     /* tile raster: cluster-tile rows that sweep N together (0 = default) */
+  int reserved[5];
 } tcx_gemm_opts;
 tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
                        const void* A, int64_t lda, const void* B, int64_t ldb,
@@ -184,6 +187,20 @@ tcx_status tcx_probe(int device, const tcx_probe_config* cfg, tcx_probe_result* 
  * M=128,N=64 tcgen05.mma with C preloaded into tensor memory. */
 tcx_status tcx_mma_tiles_tc05(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, int64_t count,
                               const void* A, const void* B, const void* C, void* D, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * tcx_mma_chain — the paper's chain matrix multiplication (Fig.
+ * code-chain-matmul; Eq. 1 PAPER.md:1028-1030 is evaluated by the caller):
+ *     D_1 = A_1 x B_1;   A_i = cvt(D_{i-1}),  D_i = A_i x B_i   (i = 2 .. n_steps)
+ * with one m16n8k8 MMA per step (the paper's shape), FP32 D, and cvt =
+ * round-to-nearest-even of FP32 into ab (FP16 overflow -> inf; TF32 as tcx_round_tf32).
+ * ab in {F16, BF16, TF32}.  A0: count x 16 x 8 (ab elements, TF32 in FP32 containers);
+ * Bs: count x n_steps x 8 x 8, stored n x k ("col") per step; Ds (out): count x n_steps x 16 x 8
+ * FP32 — every step's D, the last one being the chain's result.  count == 0 or n_steps == 0
+ * is a no-op.  Asynchronous on stream.
+ * ------------------------------------------------------------------------------------- */
+tcx_status tcx_mma_chain(tcx_dtype ab, int n_steps, int64_t count, const void* A0, const void* Bs, float* Ds,
+                         void* stream);
 
 /* ------------------------------------------------------------------------------------- */
 const char* tcx_status_string(tcx_status s);

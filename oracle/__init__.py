@@ -9,6 +9,8 @@ Definitions (cited in the C sources):
   * ``D = A x B + C`` (§II-A); "row.col": A is m x k row-major, B is stored
     n x k.
   * FP16/BF16/TF32 -> FP32: every product exact, the sum exact, ONE RNE rounding to FP32.
+  * FP16 -> FP16 (C/D FP16, the mma f16.f16.f16.f16 variant): the same exact
+    sum rounded ONCE to FP16.
   * INT8 -> INT32: exact int64 sum, two's-complement wrap to 32 bits.
   * 2:4 sparse: expand(sA, meta) then dense.
 
@@ -54,6 +56,8 @@ def lib():
         L.tcxref_quantize.argtypes = [dbl, i32, i32]; L.tcxref_quantize.restype = u32
         L.tcxref_decode.argtypes = [i32, u32]; L.tcxref_decode.restype = dbl
         L.tcxref_dot_fp.argtypes = [i32, i64, vp, vp, u32, ctypes.POINTER(dbl)]; L.tcxref_dot_fp.restype = u32
+        L.tcxref_dot_fp2.argtypes = [i32, i64, vp, vp, i32, u32, i32, i32, ctypes.POINTER(dbl)]
+        L.tcxref_dot_fp2.restype = u32
         L.tcxref_dot_s8.argtypes = [i64, vp, vp, ctypes.c_int32]; L.tcxref_dot_s8.restype = ctypes.c_int32
         L.tcxref_sum_round.argtypes = [i32, vp, vp, vp, i32, i32]; L.tcxref_sum_round.restype = u32
         L.tcxref_gemm_samples.argtypes = [i32, i64, vp, i64, vp, i64, vp, i64, i64, vp, vp, vp, vp, i32]
@@ -61,10 +65,14 @@ def lib():
         L.tcxref_sp24_expand.argtypes = [i32, i64, i64, vp, i64, vp, vp, i64]; L.tcxref_sp24_expand.restype = i64
         L.tcxref_sp24_compress.argtypes = [i32, i64, i64, vp, i64, vp, i64, vp]; L.tcxref_sp24_compress.restype = i64
         L.tcxref_tiles.argtypes = [i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]; L.tcxref_tiles.restype = i32
+        L.tcxref_tiles2.argtypes = [i32, i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]; L.tcxref_tiles2.restype = i32
         L.tcxref_model_dot.argtypes = [i32, i32, vp, vp, u32, i32, i32, i32, i32, i32, i32]
         L.tcxref_model_dot.restype = u32
         L.tcxref_model_batch.argtypes = [i32, ctypes.c_long, i32, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, i32]
         L.tcxref_model_batch.restype = i32
+        L.tcxref_model_batch2.argtypes = [i32, ctypes.c_long, i32, vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32,
+                                          vp, i32]
+        L.tcxref_model_batch2.restype = i32
         L.tcxref_seq32.argtypes = [i32, vp, vp, ctypes.c_float, i32]; L.tcxref_seq32.restype = ctypes.c_float
         _lib = L
     return _lib
@@ -96,11 +104,15 @@ def quantize_array(x: np.ndarray, fmt: int) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------- dots
-def dot_fp(ab: int, a_bits: np.ndarray, b_bits: np.ndarray, c_bits: int = 0):
-    """One FP output element: RNE_fp32(c + sum a_k b_k) exactly; returns (bits, sum|ab|+|c|)."""
+def dot_fp(ab: int, a_bits: np.ndarray, b_bits: np.ndarray, c_bits: int = 0, c_fmt: int = F32,
+           out_fmt: int = F32, rz: bool = False):
+    """One FP output element: R_out(c + sum a_k b_k) computed exactly and rounded once (RNE, or
+    toward zero if rz) into out_fmt (FP32, or FP16 for the FP16-accumulate variant); c is given
+    in c_fmt.  Returns (bits, sum|ab|+|c|)."""
     a = _c(a_bits, _NP[ab]); b = _c(b_bits, _NP[ab])
     absv = ctypes.c_double(0.0)
-    r = lib().tcxref_dot_fp(ab, a.size, _p(a), _p(b), int(c_bits) & 0xFFFFFFFF, ctypes.byref(absv))
+    r = lib().tcxref_dot_fp2(ab, a.size, _p(a), _p(b), c_fmt, int(c_bits) & 0xFFFFFFFF, out_fmt, int(rz),
+                             ctypes.byref(absv))
     return int(r), absv.value
 
 
@@ -146,14 +158,18 @@ def gemm_full(ab: int, A, B, C=None, nthreads=None):
     return out.reshape(M, N), absv.reshape(M, N)
 
 
-def tiles(ab: int, m: int, n: int, k: int, A, B, C):
-    """Batch of independent tiles: D_t = A_t B_t + C_t (layouts as tcx_mma_tiles)."""
+def tiles(ab: int, m: int, n: int, k: int, A, B, C, cd: int = F32):
+    """Batch of independent tiles: D_t = A_t B_t + C_t (layouts as tcx_mma_tiles).
+    cd = F32 (C/D FP32 bits, INT32 for S8) or F16 (C given as uint16 FP16 bits; D returned as
+    FP16 bits in uint32, = RNE_fp16 of the exact value)."""
     A = np.ascontiguousarray(A); B = np.ascontiguousarray(B)
     count = A.size // (m * k)
     Cc = np.ascontiguousarray(C) if C is not None else None
+    if Cc is not None:
+        assert Cc.itemsize == (2 if cd == F16 else 4)
     D = np.zeros(count * m * n, dtype=np.uint32)
     absv = np.zeros(count * m * n, dtype=np.float64)
-    lib().tcxref_tiles(ab, m, n, k, count, _p(A), _p(B), _p(Cc) if Cc is not None else None, _p(D), _p(absv))
+    lib().tcxref_tiles2(ab, cd, m, n, k, count, _p(A), _p(B), _p(Cc) if Cc is not None else None, _p(D), _p(absv))
     return D.reshape(count, m, n), absv.reshape(count, m, n)
 
 
@@ -191,15 +207,17 @@ def seq32(a: np.ndarray, b: np.ndarray, c: float, c_last: bool = False) -> float
 
 
 def model_batch(ab: int, a_rows, b_rows, c_bits, Ki: int, g: int, p: int, rz: bool, floor_mode=False,
-                c_after=False, emode=0, nthreads=None) -> np.ndarray:
+                c_after=False, emode=0, nthreads=None, acc_fmt: int = F32) -> np.ndarray:
     """model_dot over n rows at once (n x K element bits for a and b, n FP32 bits for c).
     emode 0: align on the actual leading bit of the largest addend; 1: on exponent sums
-    (product nominal leading exponent = e_a + e_b + 1, subnormal inputs at emin)."""
+    (product nominal leading exponent = e_a + e_b + 1, subnormal inputs at emin).
+    acc_fmt: the accumulator's format (c in and D out): FP32, or FP16 for the FP16-accumulate
+    variant (truncation window and every block rounding then use FP16's 11-bit significand)."""
     a = _c(a_rows, _NP[ab]); b = _c(b_rows, _NP[ab]); c = _c(c_bits, np.uint32)
     n, K = a.shape
     out = np.zeros(n, dtype=np.uint32)
     nt = nthreads or len(os.sched_getaffinity(0))
-    rc = lib().tcxref_model_batch(ab, n, K, _p(a), _p(b), _p(c), Ki, g, p, int(rz), int(floor_mode), int(c_after),
-                                  int(emode), _p(out), nt)
+    rc = lib().tcxref_model_batch2(ab, n, K, _p(a), _p(b), _p(c), Ki, g, p, int(rz), int(floor_mode), int(c_after),
+                                   int(emode), acc_fmt, _p(out), nt)
     assert rc == 0
     return out

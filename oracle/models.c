@@ -77,25 +77,26 @@ static term trunc_to(term t, int L, int floor_mode) {
   return t;
 }
 
-static uint32_t sum_terms(int n, const term *ts, int rz) {
-  int s[64], e[64], i, k = 0;
-  uint64_t m[64];
+static uint32_t sum_terms(int n, const term *ts, int rz, int out_fmt) {
+  int s[72], e[72], i, k = 0;
+  uint64_t m[72];
   for (i = 0; i < n; i++) {
     if (ts[i].zero) continue;
     s[k] = ts[i].sign; m[k] = ts[i].mant; e[k] = ts[i].exp; k++;
   }
-  return tcxref_sum_round(k, s, m, e, REF_F32, rz);
+  return tcxref_sum_round(k, s, m, e, out_fmt, rz);
 }
 
-static term from_f32(uint32_t b) {
-  term t = dec(REF_F32, b);
+/* the accumulator term, held in acc_fmt (FP32, or FP16 for the FP16-accumulate variant) */
+static term from_acc(uint32_t b, int acc_fmt) {
+  term t = dec(acc_fmt, b);
   if (!t.zero) t.nlead = lead_exp(t);
   t.eu = 1000;                                               /* marks the accumulator term */
   return t;
 }
 
 /* align + truncate a set of terms relative to their largest addend */
-static void align_trunc(int n, term *ts, int p, int floor_mode, int emode) {
+static void align_trunc(int n, term *ts, int p, int floor_mode, int emode, int frac_bits) {
   int i, emax = -100000, L;
   if (p < 0) return;
   for (i = 0; i < n; i++)
@@ -105,20 +106,24 @@ static void align_trunc(int n, term *ts, int p, int floor_mode, int emode) {
       if (le > emax) emax = le;
     }
   if (emax == -100000) return;
-  L = emax - 23 - p;
+  L = emax - frac_bits - p;
   for (i = 0; i < n; i++) ts[i] = trunc_to(ts[i], L, floor_mode);
 }
 
-uint32_t tcxref_model_dot2(int ab, int K, const void *a, const void *b, uint32_t c_bits,
-                           int Ki, int g, int p, int rz, int floor_mode, int c_after, int emode) {
+/* M(g, p, R, t, o) with the accumulator (c in, D out) held in acc_fmt: FP32 (frac_bits 23) or
+   FP16 (frac_bits 10, the FP16-accumulate mma variant).  The truncation window is p bits below
+   acc_fmt's significand at the block's leading exponent; each block is rounded into acc_fmt. */
+uint32_t tcxref_model_dot3(int ab, int K, const void *a, const void *b, uint32_t c_bits,
+                           int Ki, int g, int p, int rz, int floor_mode, int c_after, int emode, int acc_fmt) {
   uint32_t acc = c_bits;
   int k0, j;
+  const int frac_bits = acc_fmt == REF_F16 ? 10 : 23;
   for (k0 = 0; k0 < K; k0 += Ki) {           /* one instruction */
     int kk;
     for (kk = 0; kk < Ki && k0 + kk < K; kk += g) {   /* one block */
-      term ts[64];
+      term ts[72];
       int n = 0;
-      if (!c_after) ts[n++] = from_f32(acc);
+      if (!c_after) ts[n++] = from_acc(acc, acc_fmt);
       for (j = 0; j < g && kk + j < Ki && k0 + kk + j < K; j++) {
         int idx = k0 + kk + j;
         uint32_t ab_bits = (ab == REF_F16 || ab == REF_BF16) ? ((const uint16_t *)a)[idx] : ((const uint32_t *)a)[idx];
@@ -129,19 +134,24 @@ uint32_t tcxref_model_dot2(int ab, int K, const void *a, const void *b, uint32_t
         pr.eu = 0; pr.nlead = x.eu + y.eu + 1;
         ts[n++] = pr;
       }
-      align_trunc(n, ts, p, floor_mode, emode);
+      align_trunc(n, ts, p, floor_mode, emode, frac_bits);
       if (!c_after) {
-        acc = sum_terms(n, ts, rz);
+        acc = sum_terms(n, ts, rz, acc_fmt);
       } else {
         /* products summed exactly among themselves, then one rounding of acc + S */
-        term all[65];
+        term all[73];
         memcpy(all, ts, sizeof(term) * n);
-        all[n] = from_f32(acc);
-        acc = sum_terms(n + 1, all, rz);
+        all[n] = from_acc(acc, acc_fmt);
+        acc = sum_terms(n + 1, all, rz, acc_fmt);
       }
     }
   }
   return acc;
+}
+
+uint32_t tcxref_model_dot2(int ab, int K, const void *a, const void *b, uint32_t c_bits,
+                           int Ki, int g, int p, int rz, int floor_mode, int c_after, int emode) {
+  return tcxref_model_dot3(ab, K, a, b, c_bits, Ki, g, p, rz, floor_mode, c_after, emode, REF_F32);
 }
 
 uint32_t tcxref_model_dot(int ab, int K, const void *a, const void *b, uint32_t c_bits,
@@ -165,7 +175,7 @@ float tcxref_seq32(int K, const float *a, const float *b, float c, int c_last) {
 /* batched model evaluation over n dot products (rows of a and b: n x K element bits), threaded. */
 #include <pthread.h>
 typedef struct {
-  int ab, K; const void *a, *b; const uint32_t *c; int Ki, g, p, rz, floor_mode, c_after, emode;
+  int ab, K; const void *a, *b; const uint32_t *c; int Ki, g, p, rz, floor_mode, c_after, emode, acc_fmt;
   uint32_t *out; long s0, s1;
 } mjob;
 
@@ -174,14 +184,15 @@ static void *mworker(void *arg) {
   long i;
   size_t es = (j->ab == REF_F16 || j->ab == REF_BF16) ? 2 : 4;
   for (i = j->s0; i < j->s1; i++)
-    j->out[i] = tcxref_model_dot2(j->ab, j->K, (const char *)j->a + (size_t)i * j->K * es,
+    j->out[i] = tcxref_model_dot3(j->ab, j->K, (const char *)j->a + (size_t)i * j->K * es,
                                   (const char *)j->b + (size_t)i * j->K * es, j->c[i], j->Ki, j->g, j->p,
-                                  j->rz, j->floor_mode, j->c_after, j->emode);
+                                  j->rz, j->floor_mode, j->c_after, j->emode, j->acc_fmt);
   return NULL;
 }
 
-int tcxref_model_batch(int ab, long n, int K, const void *a, const void *b, const uint32_t *c, int Ki, int g,
-                       int p, int rz, int floor_mode, int c_after, int emode, uint32_t *out, int nthreads) {
+int tcxref_model_batch2(int ab, long n, int K, const void *a, const void *b, const uint32_t *c, int Ki, int g,
+                        int p, int rz, int floor_mode, int c_after, int emode, int acc_fmt, uint32_t *out,
+                        int nthreads) {
   pthread_t th[256];
   mjob jobs[256];
   int t;
@@ -190,10 +201,15 @@ int tcxref_model_batch(int ab, long n, int K, const void *a, const void *b, cons
   for (t = 0; t < nthreads; t++) {
     mjob *j = &jobs[t];
     j->ab = ab; j->K = K; j->a = a; j->b = b; j->c = c; j->Ki = Ki; j->g = g; j->p = p; j->rz = rz;
-    j->floor_mode = floor_mode; j->c_after = c_after; j->emode = emode; j->out = out;
+    j->floor_mode = floor_mode; j->c_after = c_after; j->emode = emode; j->acc_fmt = acc_fmt; j->out = out;
     j->s0 = n * t / nthreads; j->s1 = n * (t + 1) / nthreads;
     if (pthread_create(&th[t], NULL, mworker, j)) return -1;
   }
   for (t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
   return 0;
+}
+
+int tcxref_model_batch(int ab, long n, int K, const void *a, const void *b, const uint32_t *c, int Ki, int g,
+                       int p, int rz, int floor_mode, int c_after, int emode, uint32_t *out, int nthreads) {
+  return tcxref_model_batch2(ab, n, K, a, b, c, Ki, g, p, rz, floor_mode, c_after, emode, REF_F32, out, nthreads);
 }

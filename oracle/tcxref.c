@@ -333,15 +333,23 @@ static inline uint32_t load_elem(const void *p, int64_t i, int fmt) {
   }
 }
 
-/* D element (i,j):  a = A + i*lda (K elems), b = B + j*ldb (K elems, "col" B = N x K) */
-uint32_t tcxref_dot_fp(int ab, int64_t K, const void *a, const void *b, uint32_t c_bits, double *abs_out) {
+/* D element (i,j):  a = A + i*lda (K elems), b = B + j*ldb (K elems, "col" B = N x K)
+   General form: c given in c_fmt (FP32, or FP16 for the FP16-accumulate MMA variant of
+   PAPER.md:428-429 / Table FP16-FP16-numeric-profiling), the exact sum rounded ONCE into
+   out_fmt (FP32 or FP16) with RNE (rz = 0) or toward zero (rz = 1). */
+uint32_t tcxref_dot_fp2(int ab, int64_t K, const void *a, const void *b, int c_fmt, uint32_t c_bits,
+                        int out_fmt, int rz, double *abs_out) {
   kacc k;
   int64_t t;
   kacc_init(&k);
   for (t = 0; t < K; t++)
     kacc_add_product(&k, decode_bits(ab, load_elem(a, t, ab)), decode_bits(ab, load_elem(b, t, ab)));
-  kacc_add_value(&k, decode_bits(REF_F32, c_bits));
-  return kacc_round(&k, REF_F32, 0, abs_out);
+  kacc_add_value(&k, decode_bits(c_fmt, c_bits));
+  return kacc_round(&k, out_fmt, rz, abs_out);
+}
+
+uint32_t tcxref_dot_fp(int ab, int64_t K, const void *a, const void *b, uint32_t c_bits, double *abs_out) {
+  return tcxref_dot_fp2(ab, K, a, b, REF_F32, c_bits, REF_F32, 0, abs_out);
 }
 
 int32_t tcxref_dot_s8(int64_t K, const int8_t *a, const int8_t *b, int32_t c) {
@@ -483,8 +491,11 @@ int64_t tcxref_sp24_compress(int esize, int64_t M, int64_t K, const void *dense,
 /* tile batch (tcx_mma_tiles semantics): D_t = A_t B_t + C_t, t < count.                   */
 /* A_t: m x k row-major, B_t: n x k ("col"), C_t/D_t: m x n row-major.                      */
 /* ------------------------------------------------------------------------------------ */
-int tcxref_tiles(int ab, int m, int n, int k, int64_t count, const void *A, const void *B,
-                 const void *C, uint32_t *D, double *abs_out) {
+/* cd = REF_F32 (C/D FP32 bits; INT32 for S8) or REF_F16 (C/D stored as 16-bit FP16: the
+   FP16-accumulate mma variant, D = RNE_fp16(c + sum a*b) exactly, "converts the
+   final result to low-precision FP16 in the end"). */
+int tcxref_tiles2(int ab, int cd, int m, int n, int k, int64_t count, const void *A, const void *B,
+                  const void *C, uint32_t *D, double *abs_out) {
   int64_t t;
   int i, j;
   size_t es = (ab == REF_S8) ? 1 : ((ab == REF_F16 || ab == REF_BF16) ? 2 : 4);
@@ -493,14 +504,21 @@ int tcxref_tiles(int ab, int m, int n, int k, int64_t count, const void *A, cons
       const char *a = (const char *)A + ((size_t)t * m * k + (size_t)i * k) * es;
       const char *b = (const char *)B + ((size_t)t * n * k + (size_t)j * k) * es;
       int64_t o = t * m * n + i * n + j;
-      uint32_t cb = C ? ((const uint32_t *)C)[o] : 0u;
+      uint32_t cb = 0u;
+      if (C) cb = cd == REF_F16 ? ((const uint16_t *)C)[o] : ((const uint32_t *)C)[o];
       if (ab == REF_S8) D[o] = (uint32_t)tcxref_dot_s8(k, (const int8_t *)a, (const int8_t *)b, (int32_t)cb);
       else {
         double av = 0.0;
-        D[o] = tcxref_dot_fp(ab, k, a, b, cb, &av);
+        D[o] = tcxref_dot_fp2(ab, k, a, b, cd == REF_F16 ? REF_F16 : REF_F32, cb, cd == REF_F16 ? REF_F16 : REF_F32,
+                              0, &av);
         if (abs_out) abs_out[o] = av;
       }
     }
   }
   return 0;
+}
+
+int tcxref_tiles(int ab, int m, int n, int k, int64_t count, const void *A, const void *B,
+                 const void *C, uint32_t *D, double *abs_out) {
+  return tcxref_tiles2(ab, REF_F32, m, n, k, count, A, B, C, D, abs_out);
 }

@@ -7,6 +7,7 @@ CPU fallback: if libtcx.so is missing or a call fails, an exception is raised.
 Functions (same names as the C ABI, minus the ``tcx_`` prefix):
   mma_tiles(A, B, C, D=None)            batch of m16n8k16 / m16n8k8|16 (tf32) / m16n8k32 (s8) tiles
   mma_tiles_tc05(A, B, C, D=None)       the same tiles through tcgen05 (C preloaded in TMEM)
+  mma_chain(A0, Bs)                     the paper's chain matmul: D_i = cvt(D_{i-1}) x B_i (m16n8k8)
   gemm(A, B, C=None, D=None, ...)       dense D = A @ B^T-stored + C   (B is N x K, "col")
   sp24_compress(A_dense)                -> (vals, meta_canon)
   sp24_pack_meta(meta_canon, M, K)      -> meta_hw
@@ -28,7 +29,7 @@ F16, BF16, TF32, F32, S8, S32 = 0, 1, 2, 3, 4, 5
 _STATUS = {0: "TCX_OK", 1: "TCX_ERR_INVALID_VALUE", 2: "TCX_ERR_UNSUPPORTED", 3: "TCX_ERR_MISALIGNED",
            4: "TCX_ERR_BAD_SPARSITY", 5: "TCX_ERR_NO_DEVICE", 6: "TCX_ERR_ARCH", 7: "TCX_ERR_CUDA"}
 
-EXPORTS = ["tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
+EXPORTS = ["tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_mma_chain", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
            "tcx_sp24_meta_hw_bytes", "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_gemm_sp24_ex", "tcx_round_tf32",
            "tcx_probe",
            "tcx_status_string", "tcx_last_error", "tcx_version", "tcx_launch_count"]
@@ -41,7 +42,8 @@ class TcxError(RuntimeError):
 
 
 class GemmOpts(ctypes.Structure):
-    _fields_ = [("cta_group", ctypes.c_int), ("max_ctas", ctypes.c_int), ("reserved", ctypes.c_int * 6)]
+    _fields_ = [("cta_group", ctypes.c_int), ("max_ctas", ctypes.c_int), ("group_m", ctypes.c_int),
+                ("reserved", ctypes.c_int * 5)]
 
 
 class ProbeConfig(ctypes.Structure):
@@ -70,6 +72,7 @@ def lib():
     vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
     L.tcx_mma_tiles.argtypes = [i32, i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]
     L.tcx_mma_tiles_tc05.argtypes = [i32, i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]
+    L.tcx_mma_chain.argtypes = [i32, i32, i64, vp, vp, vp, vp]
     L.tcx_gemm.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp]
     L.tcx_gemm_ex.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64, ctypes.POINTER(GemmOpts), vp]
     L.tcx_sp24_compress.argtypes = [i32, i64, i64, vp, i64, vp, vp, vp, vp]
@@ -85,7 +88,7 @@ def lib():
     L.tcx_last_error.restype = ctypes.c_char_p
     L.tcx_version.restype = ctypes.c_char_p
     L.tcx_launch_count.restype = ctypes.c_uint64
-    for f in ("tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
+    for f in ("tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_mma_chain", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
               "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_gemm_sp24_ex", "tcx_round_tf32", "tcx_probe"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -128,15 +131,19 @@ def _dev_check(*ts):
 
 
 # ---------------------------------------------------------------------------------------- tiles
-def mma_tiles(A, B, C=None, D=None, tf32=False, tc05=False):
-    """D_t = A_t B_t + C_t for A (count, 16, k), B (count, 8, k), C/D (count, 16, 8)."""
+def mma_tiles(A, B, C=None, D=None, tf32=False, tc05=False, f16_acc=False):
+    """D_t = A_t B_t + C_t for A (count, 16, k), B (count, 8, k), C/D (count, 16, 8).
+    f16_acc: C/D are FP16 (the f16.f16.f16.f16 MMA); C, if given, must be float16."""
     _dev_check(A, B, C, D)
     ab = ab_code(A, tf32)
     count, m, k = A.shape
     n = B.shape[1]
-    cd = S32 if ab == S8 else F32
+    cd = S32 if ab == S8 else (F16 if f16_acc else F32)
+    if C is not None and cd == F16 and C.dtype != torch.float16:
+        raise ValueError("f16_acc: C must be float16")
     if D is None:
-        D = torch.empty((count, m, n), dtype=torch.int32 if cd == S32 else torch.float32, device=A.device)
+        D = torch.empty((count, m, n), dtype={S32: torch.int32, F16: torch.float16, F32: torch.float32}[cd],
+                        device=A.device)
     fn = lib().tcx_mma_tiles_tc05 if tc05 else lib().tcx_mma_tiles
     _check(fn(ab, cd, m, n, k, count, _ptr(A), _ptr(B), _ptr(C), _ptr(D), _stream(A)))
     return D
@@ -146,8 +153,22 @@ def mma_tiles_tc05(A, B, C=None, D=None, tf32=False):
     return mma_tiles(A, B, C, D, tf32=tf32, tc05=True)
 
 
+def mma_chain(A0, Bs, tf32=False, Ds=None):
+    """The paper's chain matmul: A0 (count, 16, 8), Bs (count, n_steps, 8, 8)
+    stored n x k; returns Ds (count, n_steps, 16, 8) FP32 — D_i = cvt(D_{i-1}) x B_i."""
+    _dev_check(A0, Bs, Ds)
+    ab = ab_code(A0, tf32)
+    count, n_steps = Bs.shape[0], Bs.shape[1]
+    if tuple(A0.shape) != (count, 16, 8) or tuple(Bs.shape[2:]) != (8, 8) or Bs.dtype != A0.dtype:
+        raise ValueError("mma_chain: A0 (count, 16, 8), Bs (count, n_steps, 8, 8) of one dtype")
+    if Ds is None:
+        Ds = torch.empty((count, n_steps, 16, 8), dtype=torch.float32, device=A0.device)
+    _check(lib().tcx_mma_chain(ab, n_steps, count, _ptr(A0), _ptr(Bs), _ptr(Ds), _stream(A0)))
+    return Ds
+
+
 # ---------------------------------------------------------------------------------------- GEMM
-def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0):
+def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0):
     """Dense D = A x B + C with A (M, K), B stored (N, K) ("row.col"), C/D (M, N)."""
     _dev_check(A, B, C, D)
     ab = ab_code(A, tf32)
@@ -156,7 +177,7 @@ def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0):
     cd = S32 if ab == S8 else F32
     if D is None:
         D = torch.empty((M, N), dtype=torch.int32 if cd == S32 else torch.float32, device=A.device)
-    opts = GemmOpts(cta_group, max_ctas)
+    opts = GemmOpts(cta_group, max_ctas, group_m)
     _check(lib().tcx_gemm_ex(ab, cd, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
                              _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
                              ctypes.byref(opts), _stream(A)))
@@ -198,7 +219,7 @@ def sp24_pack_meta(meta_canon, M, K, ab=F16, check=True):
     return hw
 
 
-def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0):
+def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m=0):
     """D = expand(vals, meta) x B + C; vals (M, K/2), B (N, K)."""
     _dev_check(vals, meta_hw, B, C, D)
     ab = ab_code(vals)
@@ -206,7 +227,7 @@ def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0):
     N, K = B.shape
     if D is None:
         D = torch.empty((M, N), dtype=torch.float32, device=vals.device)
-    opts = GemmOpts(cta_group, max_ctas)
+    opts = GemmOpts(cta_group, max_ctas, group_m)
     _check(lib().tcx_gemm_sp24_ex(ab, F32, M, N, K, _ptr(vals), vals.stride(0), _ptr(meta_hw), _ptr(B), B.stride(0),
                                   _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
                                   ctypes.byref(opts), _stream(vals)))

@@ -134,10 +134,11 @@ uint64_t tcx_launch_count(void) { return g_launches.load(); }
 
 tcx_status tcx_mma_tiles(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, int64_t count, const void* A, const void* B,
                          const void* C, void* D, void* stream) {
-  const bool fp = (ab == TCX_F16 || ab == TCX_BF16) && cd == TCX_F32 && m == 16 && n == 8 && k == 16;
+  const bool fp = (ab == TCX_F16 || ab == TCX_BF16) && cd == TCX_F32 && m == 16 && n == 8 && (k == 16 || k == 8);
+  const bool hh = ab == TCX_F16 && cd == TCX_F16 && m == 16 && n == 8 && (k == 16 || k == 8);
   const bool tf = ab == TCX_TF32 && cd == TCX_F32 && m == 16 && n == 8 && (k == 8 || k == 16);
   const bool i8 = ab == TCX_S8 && cd == TCX_S32 && m == 16 && n == 8 && k == 32;
-  if (!(fp || tf || i8))
+  if (!(fp || hh || tf || i8))
     return set_error(TCX_ERR_UNSUPPORTED, "tcx_mma_tiles: (ab=%d, cd=%d, m%dn%dk%d) not supported", ab, cd, m, n, k);
   if (count < 0) return set_error(TCX_ERR_INVALID_VALUE, "tcx_mma_tiles: count < 0");
   if (count == 0) return TCX_OK;
@@ -147,7 +148,22 @@ tcx_status tcx_mma_tiles(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, int64_
   DevInfo dev;
   tcx_status st = current_device(&dev);
   if (st != TCX_OK) return st;
-  return launch_tiles(ab, k, count, A, B, C, D, (cudaStream_t)stream);
+  return launch_tiles(ab, cd, k, count, A, B, C, D, (cudaStream_t)stream);
+}
+
+tcx_status tcx_mma_chain(tcx_dtype ab, int n_steps, int64_t count, const void* A0, const void* Bs, float* Ds,
+                         void* stream) {
+  if (ab != TCX_F16 && ab != TCX_BF16 && ab != TCX_TF32)
+    return set_error(TCX_ERR_UNSUPPORTED, "tcx_mma_chain: ab %d (F16, BF16 or TF32)", (int)ab);
+  if (count < 0 || n_steps < 0) return set_error(TCX_ERR_INVALID_VALUE, "tcx_mma_chain: count/n_steps < 0");
+  if (count == 0 || n_steps == 0) return TCX_OK;
+  if (!A0 || !Bs || !Ds) return set_error(TCX_ERR_INVALID_VALUE, "tcx_mma_chain: NULL operand");
+  if (!aligned16(A0) || !aligned16(Bs) || !aligned16(Ds))
+    return set_error(TCX_ERR_MISALIGNED, "tcx_mma_chain: pointers must be 16-byte aligned");
+  DevInfo dev;
+  tcx_status st = current_device(&dev);
+  if (st != TCX_OK) return st;
+  return launch_chain(ab, n_steps, count, A0, Bs, Ds, (cudaStream_t)stream);
 }
 
 tcx_status tcx_mma_tiles_tc05(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, int64_t count, const void* A,
@@ -177,10 +193,11 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
   DevInfo dev;
   st = current_device(&dev);
   if (st != TCX_OK) return st;
-  GemmArgs g{ab, M, N, K, A, lda, B, ldb, C, ldc, D, ldd, nullptr, 2, 0};
+  GemmArgs g{ab, M, N, K, A, lda, B, ldb, C, ldc, D, ldd, nullptr, 2, 0, 0};
   if (opts) {
     if (opts->cta_group) g.cta_group = opts->cta_group;
     g.max_ctas = opts->max_ctas;
+    g.group_m = opts->group_m;
   }
   if (K == 0) return launch_fill_c(g, (cudaStream_t)stream);
   return launch_gemm_dense(g, dev, (cudaStream_t)stream);
@@ -247,10 +264,11 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
   DevInfo dev;
   st = current_device(&dev);
   if (st != TCX_OK) return st;
-  GemmArgs g{ab, M, N, K, A_vals, lda_vals, B, ldb, C, ldc, D, ldd, meta_hw, 2, 0};
+  GemmArgs g{ab, M, N, K, A_vals, lda_vals, B, ldb, C, ldc, D, ldd, meta_hw, 2, 0, 0};
   if (opts) {
     if (opts->cta_group == 1 || opts->cta_group == 2) g.cta_group = opts->cta_group;
     g.max_ctas = opts->max_ctas;
+    g.group_m = opts->group_m;
   }
   if (g.cta_group == 2 && M % 256)
     return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: the CTA-pair kernel needs M %% 256 == 0 (use cta_group=1)");

@@ -21,7 +21,7 @@ constexpr int KBYTES = 128;        // K bytes per stage (one SW128 row)
 constexpr int UMMA_KBYTES = 32;    // K bytes per tcgen05.mma
 constexpr int EPI_WARPS = 4;
 constexpr int NUM_THREADS = 256;
-constexpr int GROUP_M = 8;         // raster: GROUP_M cluster-tile rows share B tiles in L2
+constexpr int GROUP_M = 8;         // default raster: GROUP_M cluster-tile rows share B tiles in L2
 
 template <int CG>
 struct Cfg {
@@ -55,13 +55,13 @@ struct Smem {
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64_t n_tiles,
+__device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64_t n_tiles, int group_m,
                                             int64_t& mt, int64_t& nt) {
-  // grouped raster: GROUP_M m-tiles x all n-tiles, m fastest inside a group
-  int64_t per_group = (int64_t)GROUP_M * n_tiles;
+  // grouped raster: group_m m-tiles x all n-tiles, m fastest inside a group
+  int64_t per_group = (int64_t)group_m * n_tiles;
   int64_t g = tile / per_group;
-  int64_t first_m = g * GROUP_M;
-  int64_t gm = m_tiles - first_m < GROUP_M ? m_tiles - first_m : GROUP_M;
+  int64_t first_m = g * group_m;
+  int64_t gm = m_tiles - first_m < group_m ? m_tiles - first_m : group_m;
   int64_t r = tile - g * per_group;
   mt = first_m + r % gm;
   nt = r / gm;
@@ -71,7 +71,7 @@ template <int CG, int KIND>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   int64_t M, int64_t N, int64_t K, const void* __restrict__ Cptr, int64_t ldc,
-                  void* __restrict__ Dptr, int64_t ldd, uint32_t idesc, int a_fmt_unused) {
+                  void* __restrict__ Dptr, int64_t ldd, uint32_t idesc, int group_m) {
   using C_ = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -107,7 +107,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       const uint32_t full0_cluster = CG == 2 ? mapa(smem_u32(&sm->full[0]), 0) : 0;
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int64_t mt, nt;
-        tile_coords(tile, m_tiles, n_tiles, mt, nt);
+        tile_coords(tile, m_tiles, n_tiles, group_m, mt, nt);
         const int arow = (int)(mt * BM * CG + rank * BM);
         const int brow = (int)(nt * BN + rank * C_::BN_LOAD);
         for (int64_t kb = 0; kb < k_blocks; ++kb) {
@@ -167,7 +167,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), 0) : smem_u32(&sm->tmem_empty[0]);
     for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
       int64_t mt, nt;
-      tile_coords(tile, m_tiles, n_tiles, mt, nt);
+      tile_coords(tile, m_tiles, n_tiles, group_m, mt, nt);
       const int64_t row = mt * BM * CG + rank * BM + e * 32 + lane;
       const int64_t col0 = nt * BN;
       mbar_wait(&sm->tmem_full[acc], acc_phase);
@@ -275,7 +275,8 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
   cfg.attrs = attr; cfg.numAttrs = 1;
   const uint32_t idesc = make_idesc(KIND, a_fmt, BM * CG, BN);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K, a.C,
-                                  (int64_t)a.ldc, a.D, (int64_t)a.ldd, idesc, 0));
+                                  (int64_t)a.ldc, a.D, (int64_t)a.ldd, idesc,
+                                  a.group_m > 0 ? a.group_m : GROUP_M));
   count_launch();
   return TCX_OK;
 }

@@ -22,7 +22,7 @@ constexpr int ACC_STRIDE = 256;    // TMEM column offset between the two accumul
 constexpr int META_COL = 496;      // metadata ring: 4 slots x 4 columns
 constexpr int NUM_THREADS = 256;
 constexpr int EPI_WARPS = 4;
-constexpr int GROUP_M = 8;
+constexpr int GROUP_M = 8;            // default raster group (cluster-tile rows sweeping N together)
 constexpr int KL = 128;            // logical K per stage
 constexpr int META_BYTES = 2048;   // one 128-row x 128-logical-K metadata atom
 
@@ -47,11 +47,12 @@ struct Smem {
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64_t n_tiles, int64_t& mt, int64_t& nt) {
-  int64_t per_group = (int64_t)GROUP_M * n_tiles;
+__device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64_t n_tiles, int group_m,
+                                            int64_t& mt, int64_t& nt) {
+  int64_t per_group = (int64_t)group_m * n_tiles;
   int64_t g = tile / per_group;
-  int64_t first_m = g * GROUP_M;
-  int64_t gm = m_tiles - first_m < GROUP_M ? m_tiles - first_m : GROUP_M;
+  int64_t first_m = g * group_m;
+  int64_t gm = m_tiles - first_m < group_m ? m_tiles - first_m : group_m;
   int64_t r = tile - g * per_group;
   mt = first_m + r % gm;
   nt = r / gm;
@@ -61,7 +62,8 @@ template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmE, int64_t M, int64_t N, int64_t K,
-                 const float* __restrict__ Cptr, int64_t ldc, float* __restrict__ Dptr, int64_t ldd, uint32_t idesc) {
+                 const float* __restrict__ Cptr, int64_t ldc, float* __restrict__ Dptr, int64_t ldd, uint32_t idesc,
+                 int group_m) {
   using C_ = SpCfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -95,7 +97,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       const uint32_t full0_cluster = CG == 2 ? mapa(smem_u32(&sm->full[0]), 0) : 0;
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int64_t mt, nt;
-        tile_coords(tile, m_tiles, n_tiles, mt, nt);
+        tile_coords(tile, m_tiles, n_tiles, group_m, mt, nt);
         const int64_t mrow = mt * BM * CG + rank * BM;
         const int brow = (int)(nt * BN + rank * C_::BN_LOAD);
         const int64_t mb = mrow / 128;
@@ -167,7 +169,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), 0) : smem_u32(&sm->tmem_empty[0]);
     for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
       int64_t mt, nt;
-      tile_coords(tile, m_tiles, n_tiles, mt, nt);
+      tile_coords(tile, m_tiles, n_tiles, group_m, mt, nt);
       const int64_t row = mt * BM * CG + rank * BM + e * 32 + lane;
       const int64_t col0 = nt * BN;
       mbar_wait(&sm->tmem_full[acc], acc_phase);
@@ -250,7 +252,8 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   const uint32_t idesc = (1u << 2) | (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
                          ((uint32_t)((BM * CG) >> 4) << 24);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tE, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K, (const float*)a.C,
-                                  (int64_t)a.ldc, (float*)a.D, (int64_t)a.ldd, idesc));
+                                  (int64_t)a.ldc, (float*)a.D, (int64_t)a.ldd, idesc,
+                                  a.group_m > 0 ? a.group_m : GROUP_M));
   count_launch();
   return TCX_OK;
 }

@@ -33,10 +33,13 @@ tcx_status make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* ba
   } while (0)
 
 // ---- launchers (validated arguments) ----
-tcx_status launch_tiles(tcx_dtype ab, int k, int64_t count, const void* A, const void* B,
+tcx_status launch_tiles(tcx_dtype ab, tcx_dtype cd, int k, int64_t count, const void* A, const void* B,
                         const void* C, void* D, cudaStream_t s);
 tcx_status launch_tiles_tc05(tcx_dtype ab, int k, int64_t count, const void* A, const void* B,
                              const void* C, void* D, cudaStream_t s);
+
+tcx_status launch_chain(tcx_dtype ab, int n_steps, int64_t count, const void* A0, const void* Bs, float* Ds,
+                        cudaStream_t s);
 
 struct GemmArgs {
   tcx_dtype ab;
@@ -48,6 +51,7 @@ struct GemmArgs {
   const void* meta_hw;   // sparse only
   int cta_group;
   int max_ctas;
+  int group_m;    // 0 = default
 };
 tcx_status launch_gemm_dense(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);
 tcx_status launch_gemm_sp24(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);

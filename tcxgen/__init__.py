@@ -337,3 +337,114 @@ def probe_classes(fmt, n_per_class=8192, seed=0):
     C[:, 0, 0] = c.to(torch.float32)
     return {"A": to_format(A, fmt), "B": to_format(B, fmt), "C": C, "cls": cls, "ptype": ptype,
             "a32": a32.to(torch.float32), "b32": b32.to(torch.float32), "c32": c32.to(torch.float32), "K": K}
+
+
+# ----------------------------------------------------------------------------------------------
+# FP16-accumulate numeric probe: the mma f16.f16.f16.f16 variant
+# probed like Table FP16-FP16-numeric-profiling.  The
+# crafted classes of configs[1] rescaled to FP16's range (c = 2^11 is where ulp(c) = 2, as 2^24 is
+# for FP32); d00 only, values in row 0 of A / column 0 of B / c00.
+# ----------------------------------------------------------------------------------------------
+CLASSES_F16ACC = ("SPREAD16", "CANCEL16", "BIGC16", "LADDER16", "TIES16", "PAPER3_init_FP16", "PAPER3_init_FP32")
+
+
+def probe_classes_f16acc(n_per_class=8192, seed=0):
+    """returns dict: A (T,16,16) f16, B (T,8,16) f16, C (T,16,8) f16, cls, ptype (PROBE_TYPES index,
+    -1 for crafted), a32/b32/c32: the FP32 values of the paper's CPU baseline."""
+    K = 16
+    T = n_per_class * len(CLASSES_F16ACC)
+    a = torch.zeros(T, K, dtype=torch.float64)
+    b = torch.zeros(T, K, dtype=torch.float64)
+    c = torch.zeros(T, dtype=torch.float64)
+    a32 = torch.zeros(T, K, dtype=torch.float64)
+    b32 = torch.zeros(T, K, dtype=torch.float64)
+    c32 = torch.zeros(T, dtype=torch.float64)
+    ptype = torch.full((T,), -1, dtype=torch.int64)
+    cls = torch.arange(T) // n_per_class
+    n = n_per_class
+
+    def sig(u):
+        return 1.0 + torch.floor(u * 1024) / 1024
+
+    def sgn(u):
+        return torch.where(u < 0.5, -1.0, 1.0).double()
+
+    def split(e, ua, ub, us):
+        ea = torch.clamp(torch.floor(e / 2.0), min=-14)
+        eb = e - ea
+        return sgn(us) * sig(ua) * torch.pow(2.0, ea), sig(ub) * torch.pow(2.0, eb)
+
+    for ci, name in enumerate(CLASSES_F16ACC):
+        s = slice(ci * n, (ci + 1) * n)
+        st = 48 + ci
+        U = _u(seed, st, n, 8 * K)
+        if name == "SPREAD16":
+            e = torch.floor(U[:, 0:K] * 19) - 14                   # product exponents in [-14, 4]
+            a[s], b[s] = split(e, U[:, K:2 * K], U[:, 2 * K:3 * K], U[:, 3 * K:4 * K])
+        elif name == "CANCEL16":
+            e = torch.floor(U[:, 0:K] * 6) - 3
+            x, y = split(e, U[:, K:2 * K], U[:, 2 * K:3 * K], U[:, 3 * K:4 * K])
+            x[:, 1::2] = -x[:, 0::2]
+            y[:, 1::2] = y[:, 0::2]
+            er = -(4 + torch.floor(U[:, 4 * K] * 11))              # residual 2^-4 .. 2^-14
+            rx, ry = split(er.unsqueeze(1), U[:, 5 * K:5 * K + 1], U[:, 5 * K + 1:5 * K + 2], U[:, 5 * K + 2:5 * K + 3])
+            x[:, 14:15], y[:, 14:15] = rx, ry
+            x[:, 15], y[:, 15] = 0.0, 0.0
+            a[s], b[s] = x, y
+            c[s] = to_format(normal(seed, st + 64, 0, n).double(), "f16").double()
+        elif name == "BIGC16":
+            m = torch.floor(U[:, 6 * K] * 1024)
+            c[s] = sgn(U[:, 6 * K + 1]) * 2048.0 * (1 + m / 1024)  # [2^11, 2^12): ulp 2
+            e = torch.floor(U[:, 0:K] * 11) - 9                    # products 2^-9 .. 2^1
+            a[s], b[s] = split(e, U[:, K:2 * K], U[:, 2 * K:3 * K], U[:, 3 * K:4 * K])
+        elif name == "LADDER16":
+            j = torch.floor(U[:, 0] * 11)                          # 16 equal products 2^-j
+            ea = -torch.floor(j / 2)
+            a[s] = torch.pow(2.0, ea).unsqueeze(1).expand(n, K)
+            b[s] = torch.pow(2.0, -j - ea).unsqueeze(1).expand(n, K)
+            c[s] = 2048.0
+        elif name == "TIES16":
+            t = torch.floor(U[:, 0] * 512)
+            c[s] = sgn(U[:, 1]) * (2048.0 + 2 * t)                 # ulp(c) = 2: a product of +-1 is a tie
+            v = torch.floor(U[:, 2] * 3)
+            x = torch.zeros(n, K, dtype=torch.float64)
+            y = torch.zeros(n, K, dtype=torch.float64)
+            pm = sgn(U[:, 3])
+            x[:, 0] = pm
+            y[:, 0] = 1.0
+            sel = v == 1
+            x[sel, 0] = pm[sel] * 0.5
+            x[sel, 1] = pm[sel] * 0.5
+            y[sel, 1] = 1.0
+            sel = v == 2
+            j = 4 + torch.floor(U[:, 4] * 8)                       # 2^-4 .. 2^-11 nudges
+            x[sel, 1] = (sgn(U[:, 5]) * torch.pow(2.0, -j))[sel]
+            y[sel, 1] = 1.0
+            a[s], b[s] = x, y
+        else:   # the paper's three probes, N(0,1), c0 FP16 (init_FP16) or converted at copy (init_FP32)
+            z = normal(seed, 48 + 5, 0, 5 * n).view(n, 5).double()
+            z32 = z.to(torch.float32).double()
+            pt = torch.arange(n) % 3
+            x = torch.zeros(n, K, dtype=torch.float64)
+            y = torch.zeros(n, K, dtype=torch.float64)
+            cc = torch.zeros(n, dtype=torch.float64)
+            x[:, 0], y[:, 0] = z32[:, 0], z32[:, 1]
+            inner = pt == 1
+            x[inner, 1], y[inner, 1] = z32[inner, 2], z32[inner, 3]
+            acc = pt == 2
+            cc[acc] = z32[acc, 4]
+            ptype[s] = pt
+            if name == "PAPER3_init_FP16":
+                x = to_format(x, "f16").double()
+                y = to_format(y, "f16").double()
+                cc = to_format(cc, "f16").double()
+            a32[s], b32[s], c32[s] = x, y, cc
+            a[s], b[s], c[s] = x, y, cc
+    A = torch.zeros(T, 16, K, dtype=torch.float16)
+    B = torch.zeros(T, 8, K, dtype=torch.float16)
+    C = torch.zeros(T, 16, 8, dtype=torch.float16)
+    A[:, 0, :] = to_format(a, "f16")
+    B[:, 0, :] = to_format(b, "f16")
+    C[:, 0, 0] = to_format(c, "f16")
+    return {"A": A, "B": B, "C": C, "cls": cls, "ptype": ptype, "a32": a32.float(), "b32": b32.float(),
+            "c32": c32.float(), "K": K}

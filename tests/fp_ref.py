@@ -73,3 +73,46 @@ def rne_bits_generic(x: Fraction, P: int, emin: int, emax: int):
     if fl >= 2 ** (P - 1) and qexp + P - 1 > emax:
         return "inf"
     return sign, fl, qexp
+
+
+F16_OVF = Fraction(65504 + 16)                 # >= this rounds to inf under RNE (65504 has an odd significand)
+
+
+def f16_bits_of(x: float) -> int:
+    return int(np.array([x], dtype=np.float16).view(np.uint16)[0])
+
+
+def f16_from_bits(b: int) -> np.float16:
+    return np.array([b & 0xFFFF], dtype=np.uint16).view(np.float16)[0]
+
+
+def rne_f16_bits(x: Fraction, rz: bool = False) -> int:
+    """RNE (or round-toward-zero) of an exact rational into binary16 by nearest-neighbour search
+    over numpy float16 candidates, with exact Fraction comparisons."""
+    if x == 0:
+        return 0
+    sign = 1 if x < 0 else 0
+    ax = -x if x < 0 else x
+    if not rz and ax >= F16_OVF:
+        return (sign << 15) | 0x7C00
+    if rz and ax >= Fraction(65504):
+        return (sign << 15) | 0x7BFF
+    g = np.float16(min(float(ax), 65504.0))
+    for _ in range(3):
+        g = np.nextafter(g, np.float16(0))
+    cands = []
+    for _ in range(7):
+        if np.isfinite(g):
+            cands.append(f16_bits_of(float(g)))
+        g = np.nextafter(g, np.float16(np.inf))
+    best = None
+    for b in sorted(set(cands)):
+        v = Fraction(float(f16_from_bits(b)))
+        if rz:
+            if v <= ax and (best is None or v > best[0]):
+                best = (v, b)
+        else:
+            key = (abs(v - ax), b & 1)
+            if best is None or key < best[0]:
+                best = (key, b)
+    return best[1] | (sign << 15)

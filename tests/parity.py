@@ -76,3 +76,25 @@ def check_gemm_samples(ab, A, B, C, D, rows, cols, K, what=""):
         assert mism.size == 0, f"{what}: {mism.size} int mismatches, first at {(rows[mism[0]], cols[mism[0]])}"
         return 0.0
     return fp_bound_check(got, ref, absv, K, what)
+
+
+def fp16_bound_check(got_bits: np.ndarray, ref_bits: np.ndarray, absv: np.ndarray, K: int, what=""):
+    """FP16-accumulate bar (DESIGN.md R-F16): D_ref = RNE_fp16(exact); the hardware may differ by
+    its internal FP32-level sum error (the north_star term) plus the final conversion into FP16,
+    at most 1.5 FP16 ulps from D_ref whatever the rounding mode; the bar allows 2 ulps:
+        |D - D_ref| <= 2 * max(2^-10 |D_ref|, 2^-24) + (K + 2) * 2^-23 * (sum|ab| + |c|).
+    Returns the max error in FP16 ulps of D_ref."""
+    got = got_bits.astype(np.uint16).view(np.float16).astype(np.float64)
+    ref = ref_bits.astype(np.uint16).view(np.float16).astype(np.float64)
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isfinite(got), fin), f"{what}: finiteness differs"
+    got, ref, absv = got[fin], ref[fin], absv[fin]
+    ulp = np.maximum(2.0 ** -10 * np.abs(ref), 2.0 ** -24)
+    err = np.abs(got - ref)
+    bound = 2 * ulp + (K + 2) * 2.0 ** -23 * absv
+    bad = err > bound
+    if bad.any():
+        i = int(np.argmax(bad))
+        raise AssertionError(f"{what}: {int(bad.sum())} elements exceed the FP16 bar; first: got {got[i]!r} "
+                             f"ref {ref[i]!r} bound {bound[i]!r}")
+    return float((err / ulp).max()) if err.size else 0.0

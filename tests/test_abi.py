@@ -40,8 +40,10 @@ def test_host_only_calls_without_gpu():
     assert L.tcx_version().startswith(b"tcx")
     # pure-host size query and argument validation return before any device work
     assert tcx.sp24_meta_hw_bytes(256, 1024) == 256 * 1024 // 8
-    st = L.tcx_mma_tiles(0, 3, 16, 8, 8, 1, None, None, None, None, None)    # bad shape
+    st = L.tcx_mma_tiles(0, 3, 16, 8, 4, 1, None, None, None, None, None)    # bad shape
     assert st == 2
+    assert L.tcx_mma_chain(4, 3, 1, None, None, None, None) == 2              # S8 chain: unsupported
+    assert L.tcx_mma_chain(0, 3, 0, None, None, None, None) == 0              # count 0: no-op
     st = L.tcx_gemm(4, 3, 16, 16, 16, None, 16, None, 16, None, 16, None, 16, None)   # s8 -> f32 unsupported
     assert st == 2
 

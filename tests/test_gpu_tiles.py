@@ -6,7 +6,7 @@ import torch
 import oracle as O
 import tcxgen
 import paper_2206_02874_b200 as tcx
-from parity import host_bits, fp_bound_check
+from parity import host_bits, fp_bound_check, fp16_bound_check
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
@@ -82,7 +82,65 @@ def test_tiles_no_c_and_empty_and_determinism():
 
 
 def test_tiles_unsupported_shape_raises():
-    A = torch.zeros((4, 16, 8), dtype=torch.float16, device=DEV)
-    B = torch.zeros((4, 8, 8), dtype=torch.float16, device=DEV)
+    A = torch.zeros((4, 16, 4), dtype=torch.float16, device=DEV)
+    B = torch.zeros((4, 8, 4), dtype=torch.float16, device=DEV)
     with pytest.raises(tcx.TcxError):
         tcx.mma_tiles(A, B, None)
+    A = torch.zeros((4, 16, 16), dtype=torch.bfloat16, device=DEV)
+    B = torch.zeros((4, 8, 16), dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(tcx.TcxError):               # FP16 accumulate exists for FP16 inputs only
+        tcx.mma_tiles(A, B, None, f16_acc=True)
+
+
+@pytest.mark.parametrize("fmt", ["f16", "bf16"])
+@pytest.mark.parametrize("count", [1, 9, 3000])
+def test_tiles_m16n8k8_f32(fmt, count):
+    """m16n8k8 (the chain-matmul shape) with FP32 C/D."""
+    A, B, C = _tiles_problem(count, fmt, seed=40 + count, k=8)
+    D = tcx.mma_tiles(A, B, C)
+    torch.cuda.synchronize()
+    _check(fmt, A, B, C, D, 8)
+
+
+def _f16acc_problem(count, k, seed, scale=1.0):
+    A = tcxgen.normal_matrix((count, 16, k), "f16", seed, tcxgen.STREAM_A, DEV)
+    B = tcxgen.normal_matrix((count, 8, k), "f16", seed, tcxgen.STREAM_B, DEV)
+    C = (tcxgen.normal_matrix((count, 16, 8), "f32", seed, tcxgen.STREAM_C, DEV) * scale).to(torch.float16)
+    return A, B, C
+
+
+@pytest.mark.parametrize("k", [16, 8])
+@pytest.mark.parametrize("count", [1, 7, 4097])
+def test_tiles_fp16_accumulate_vs_oracle(k, count):
+    """(F16, F16) tiles: D = A B + C with FP16 C/D vs RNE_fp16(exact)."""
+    A, B, C = _f16acc_problem(count, k, seed=count + k)
+    D = tcx.mma_tiles(A, B, C, f16_acc=True)
+    torch.cuda.synchronize()
+    assert D.dtype == torch.float16
+    ref, absv = O.tiles(O.F16, 16, 8, k, host_bits(A), host_bits(B), host_bits(C), cd=O.F16)
+    fp16_bound_check(host_bits(D).reshape(ref.shape), ref, absv, k, f"f16acc k{k}")
+
+
+def test_tiles_fp16_accumulate_integer_bit_exact_and_no_c():
+    """integer-valued FP16 inputs with |sum| < 2048: every partial and the result are exact FP16
+    values, so D must equal the oracle bit for bit; C = NULL means zeros."""
+    count = 2048
+    A = tcxgen.int32_matrix((count, 16, 16), 3, 1, -4, 4, DEV).to(torch.float16)
+    B = tcxgen.int32_matrix((count, 8, 16), 3, 2, -4, 4, DEV).to(torch.float16)
+    C = tcxgen.int32_matrix((count, 16, 8), 3, 3, -1000, 1000, DEV).to(torch.float16)
+    for Cx in (C, None):
+        D = tcx.mma_tiles(A, B, Cx, f16_acc=True)
+        torch.cuda.synchronize()
+        ref, _ = O.tiles(O.F16, 16, 8, 16, host_bits(A), host_bits(B), host_bits(Cx) if Cx is not None else None,
+                         cd=O.F16)
+        assert np.array_equal(host_bits(D).reshape(ref.shape).astype(np.uint32), ref)
+
+
+def test_tiles_fp16_accumulate_overflow_is_inf():
+    """FP16 range: 8 products of 128*128 = 2^17 > 65504 must give +inf (the chain-matmul
+    overflow the paper reports for FP16), as the oracle does."""
+    A = torch.full((4, 16, 8), 128.0, dtype=torch.float16, device=DEV)
+    B = torch.full((4, 8, 8), 128.0, dtype=torch.float16, device=DEV)
+    D = tcx.mma_tiles(A, B, None, f16_acc=True)
+    torch.cuda.synchronize()
+    assert torch.isinf(D).all() and (D > 0).all()
