@@ -304,6 +304,29 @@ def time_e2e(work, steps, warmup):
     return e0.elapsed_time(e1) / steps
 
 
+def tiles_steady_state(tcx, dev, count=524288, reps=10):
+    """C1's kernel at steady state: one launch over 524,288 m16n8k16 FP16 tiles (940 MB > L2),
+    CUDA events over `reps` launches; the C1 line itself is a 7 MB launch bound by launch latency."""
+    import tcxgen as g
+    A = g.uniform_matrix((count, 16, 16), "f16", 1, g.STREAM_A, device=dev)
+    B = g.uniform_matrix((count, 8, 16), "f16", 1, g.STREAM_B, device=dev)
+    C = g.uniform_matrix((count, 16, 8), "f32", 1, g.STREAM_C, device=dev)
+    D = torch.empty(count, 16, 8, device=dev)
+    for _ in range(3):
+        tcx.mma_tiles(A, B, C, D)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        tcx.mma_tiles(A, B, C, D)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    gbs = 1792.0 * count / (us * 1e-6) / 1e9
+    return {"tiles": count, "us_per_launch": round(us, 2), "GB/s": round(gbs, 1),
+            "frac_of_hbm": round(gbs / peaks()["hbm"], 4)}
+
+
 def roofline(work, ms, pk):
     if work.bound == "hbm":
         ach = work.alg_bytes / (ms * 1e-3) / 1e9
@@ -522,10 +545,16 @@ def main():
         for extra in ("c3tf32", "c4", "c5", "c1"):
             try:
                 w2 = Work(extra, 0, 1, dev)
-                ms2, l2, _, _ = time_steps(w2, max(5, min(args.steps, 20)), 3, False)
+                sampler.samples = []
+                sampler.start()
+                ms2, l2, u0, u1 = time_steps(w2, max(5, min(args.steps, 20)), 3, False)
+                sampler.stop()
                 v2 = w2.metric_value(ms2 * 1e-3)
                 also[extra] = {"workload": cfg_names[extra], "value": round(v2, 3), "unit": w2.unit,
-                               "ms_per_step": round(ms2, 5), "roofline": roofline(w2, ms2, pk), "gpu_launches": l2}
+                               "ms_per_step": round(ms2, 5), "roofline": roofline(w2, ms2, pk), "gpu_launches": l2,
+                               "clocks": sampler.summary(u0, u1)}
+                if extra == "c1":
+                    also[extra]["steady_state"] = tiles_steady_state(w2.tcx, dev)
                 del w2
                 torch.cuda.empty_cache()
             except Exception as e:  # report, never hide

@@ -74,6 +74,8 @@ def lib():
                                           vp, i32]
         L.tcxref_model_batch2.restype = i32
         L.tcxref_seq32.argtypes = [i32, vp, vp, ctypes.c_float, i32]; L.tcxref_seq32.restype = ctypes.c_float
+        L.tcxref_quantize_f32_bits.argtypes = [i32, i64, vp, vp]; L.tcxref_quantize_f32_bits.restype = None
+        L.tcxref_chain_fp32.argtypes = [i64, i32, vp, vp, vp]; L.tcxref_chain_fp32.restype = None
         _lib = L
     return _lib
 
@@ -221,3 +223,22 @@ def model_batch(ab: int, a_rows, b_rows, c_bits, Ki: int, g: int, p: int, rz: bo
                                    int(emode), acc_fmt, _p(out), nt)
     assert rc == 0
     return out
+
+
+# ---------------------------------------------------------------------------- chain matmul
+def quantize_f32_bits(bits32: np.ndarray, fmt: int) -> np.ndarray:
+    """FP32 bits -> fmt bits (RNE), elementwise: the chain's D_{i-1} -> A_i conversion."""
+    x = _c(bits32, np.uint32)
+    out = np.zeros(x.size, dtype=np.uint32)
+    lib().tcxref_quantize_f32_bits(fmt, x.size, _p(x), _p(out))
+    return out.astype(_NP[fmt] if fmt != S8 else np.uint32).reshape(np.shape(bits32))
+
+
+def chain_fp32(A0: np.ndarray, Bs: np.ndarray) -> np.ndarray:
+    """The paper's CPU FP32 chain: A0 (count,16,8) float32, Bs
+    (count,n_steps,8,8) float32 stored n x k; returns every D_i (count,n_steps,16,8) float32."""
+    A0 = _c(A0, np.float32); Bs = _c(Bs, np.float32)
+    count, n_steps = Bs.shape[0], Bs.shape[1]
+    Ds = np.zeros((count, n_steps, 16, 8), dtype=np.float32)
+    lib().tcxref_chain_fp32(count, n_steps, _p(A0), _p(Bs), _p(Ds))
+    return Ds

@@ -522,3 +522,43 @@ int tcxref_tiles(int ab, int m, int n, int k, int64_t count, const void *A, cons
                  const void *C, uint32_t *D, double *abs_out) {
   return tcxref_tiles2(ab, REF_F32, m, n, k, count, A, B, C, D, abs_out);
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* chain matrix multiplication (Fig. code-chain-matmul)              */
+/* ------------------------------------------------------------------------------------ */
+/* FP32 bits -> fmt bits, RNE (the chain's conversion of D_{i-1} into the next A_i). */
+void tcxref_quantize_f32_bits(int fmt, int64_t n, const uint32_t *in, uint32_t *out) {
+  int64_t i;
+  for (i = 0; i < n; i++) {
+    float f;
+    memcpy(&f, &in[i], 4);
+    out[i] = tcxref_quantize((double)f, fmt, 0);
+  }
+}
+
+/* The paper's CPU baseline "D^FP32": the same chain computed on the CPU in
+   binary32 — D_i = A_i x B_i with each element a sequential binary32 dot (ascending k, no FMA
+   contraction: built with -ffp-contract=off), and A_{i+1} = D_i with no conversion.
+   A0: count x 16 x 8 floats; Bs: count x n_steps x 8 x 8 (n x k); Ds: count x n_steps x 16 x 8. */
+void tcxref_chain_fp32(int64_t count, int n_steps, const float *A0, const float *Bs, float *Ds) {
+  int64_t c;
+  for (c = 0; c < count; c++) {
+    float a[16 * 8];
+    int s, i, j, k;
+    memcpy(a, A0 + c * 128, sizeof(a));
+    for (s = 0; s < n_steps; s++) {
+      const float *b = Bs + (c * n_steps + s) * 64;
+      float *d = Ds + (c * n_steps + s) * 128;
+      for (i = 0; i < 16; i++)
+        for (j = 0; j < 8; j++) {
+          float acc = 0.0f;
+          for (k = 0; k < 8; k++) {
+            volatile float p = a[i * 8 + k] * b[j * 8 + k];
+            acc = acc + p;
+          }
+          d[i * 8 + j] = acc;
+        }
+      memcpy(a, d, sizeof(a));
+    }
+  }
+}

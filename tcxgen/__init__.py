@@ -448,3 +448,25 @@ def probe_classes_f16acc(n_per_class=8192, seed=0):
     C[:, 0, 0] = to_format(c, "f16")
     return {"A": A, "B": B, "C": C, "cls": cls, "ptype": ptype, "a32": a32.float(), "b32": b32.float(),
             "c32": c32.float(), "K": K}
+
+
+# ----------------------------------------------------------------------------------------------
+# Chain matrix multiplication: "All values are randomly
+# generated by normal distribution with mu = 0 and sigma = 1" (Fig. chain-result caption).
+# init "low": values created in the low-precision type, so the CPU FP32 baseline uses the same
+# values; init "fp32": values created in FP32 and converted when copied to the GPU.
+# ----------------------------------------------------------------------------------------------
+CHAIN_STREAM = 96
+
+
+def chain_problem(fmt, count, n_steps, init="low", seed=0):
+    """returns (A0_gpu, Bs_gpu) in fmt's storage (TF32 in FP32) and (A0_cpu, Bs_cpu) float32:
+    A0 (count, 16, 8), Bs (count, n_steps, 8, 8) stored n x k."""
+    a = normal(seed, CHAIN_STREAM, 0, count * 128).view(count, 16, 8).to(torch.float32)
+    b = normal(seed, CHAIN_STREAM + 1, 0, count * n_steps * 64).view(count, n_steps, 8, 8).to(torch.float32)
+    a_low, b_low = to_format(a.double(), fmt), to_format(b.double(), fmt)
+    if init == "low":
+        return a_low, b_low, a_low.to(torch.float32), b_low.to(torch.float32)
+    if init == "fp32":
+        return a_low, b_low, a, b
+    raise ValueError(init)

@@ -1,0 +1,122 @@
+"""Chain matrix multiplication through tcx_mma_chain.
+
+Parity, every step of every chain: D_1 vs the oracle's exact tile result for (A_1, B_1); for i > 1
+the oracle converts the GPU's own D_{i-1} into A_i (RNE, oracle.quantize_f32_bits) and D_i must be
+within the north_star FP bound (K = 8) of the oracle's exact A_i x B_i.  A wrong conversion
+(rounding mode, lane mapping) moves D_i by ~ulp(low format) * sum|ab| >> the FP32-level bound, so
+this also checks the in-register D -> A conversion.  Non-finite results (FP16 overflow) must match
+the oracle's class (inf of the same sign, or NaN).
+
+Report (the paper's Fig. chain-result): Eq. 1 relative L2 error of the GPU chain vs the paper's
+CPU FP32 chain (oracle.chain_fp32), averaged over 1000 chains ("The errors are taken on average with
+1000 measurements"), chain length N = 1..20, TF32 / BF16 / FP16, init low-precision vs FP32;
+written to $TCX_REPORT_DIR/chain_matmul_report.json."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import tcxgen
+import paper_2206_02874_b200 as tcx
+from parity import host_bits
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+FMT = {"f16": O.F16, "bf16": O.BF16, "tf32": O.TF32}
+TORCH = {"f16": torch.float16, "bf16": torch.bfloat16, "tf32": torch.float32}
+
+
+def _run(fmt, count, n_steps, init, seed=0):
+    a, b, a32, b32 = tcxgen.chain_problem(fmt, count, n_steps, init, seed)
+    A0, Bs = a.to(DEV), b.to(DEV)
+    Ds = tcx.mma_chain(A0, Bs, tf32=(fmt == "tf32"))
+    torch.cuda.synchronize()
+    return A0, Bs, Ds, a32, b32
+
+
+def _check_steps(fmt, A0, Bs, Ds):
+    ab = FMT[fmt]
+    count, n_steps = Bs.shape[0], Bs.shape[1]
+    Dh = host_bits(Ds)                                   # (count, n_steps, 16, 8) FP32 bits
+    Bh = host_bits(Bs)
+    A = host_bits(A0)
+    worst = 0.0
+    for s in range(n_steps):
+        ref, absv = O.tiles(ab, 16, 8, 8, A, Bh[:, s], None)
+        got = Dh[:, s].view(np.float32).astype(np.float64)
+        want = ref.view(np.float32).astype(np.float64)
+        fin = np.isfinite(want)
+        assert np.array_equal(np.isfinite(got), fin), f"{fmt} step {s}: finiteness differs"
+        nonfin = ~fin
+        assert np.array_equal(np.isnan(got[nonfin]), np.isnan(want[nonfin]))
+        assert np.array_equal(got[nonfin & ~np.isnan(want)], want[nonfin & ~np.isnan(want)])
+        err = np.abs(got[fin] - want[fin])
+        scale = 2.0 ** -23 * absv[fin]
+        assert np.all(err <= 10 * scale), f"{fmt} step {s}: {int((err > 10 * scale).sum())} beyond the bound"
+        with np.errstate(divide="ignore", invalid="ignore"):
+            worst = max(worst, float(np.nanmax(np.where(scale > 0, err / scale, 0.0))) if err.size else 0.0)
+        A = O.quantize_f32_bits(Dh[:, s], ab)           # the next A_i, from the GPU's own D_i
+    return worst
+
+
+@pytest.mark.parametrize("fmt", ["f16", "bf16", "tf32"])
+@pytest.mark.parametrize("init", ["low", "fp32"])
+def test_chain_every_step_vs_oracle(fmt, init):
+    A0, Bs, Ds, _, _ = _run(fmt, 96, 20, init, seed=1)
+    _check_steps(fmt, A0, Bs, Ds)
+
+
+def test_chain_ragged_count_and_noop():
+    A0, Bs, Ds, _, _ = _run("bf16", 13, 3, "low", seed=2)
+    _check_steps("bf16", A0, Bs, Ds)
+    E = tcx.mma_chain(A0[:0], Bs[:0])
+    assert E.shape[0] == 0
+
+
+def test_chain_fp16_overflows_like_the_paper():
+    """FP16's range: N(0,1) 8x8 chains grow ~ sqrt(8)^N, so the FP16 conversion overflows to inf
+    around N = 10; BF16/TF32 (8 exponent bits) stay finite."""
+    _, _, D16, _, _ = _run("f16", 1000, 20, "low")
+    _, _, Db16, _, _ = _run("bf16", 1000, 20, "low")
+    inf16 = (~torch.isfinite(D16)).flatten(2).any(-1).float().mean(0).cpu().numpy()
+    assert inf16[:6].max() == 0.0 and inf16[-1] > 0.5
+    assert torch.isfinite(Db16).all()
+
+
+def _eq1(Dl, D32):
+    """Eq. 1: ||D^l - D^FP32||_2 / ||D^l||_2 over the m x n matrix, per chain."""
+    num = np.sqrt(((Dl - D32) ** 2).sum(axis=(-2, -1)))
+    den = np.sqrt((Dl ** 2).sum(axis=(-2, -1)))
+    return num / den
+
+
+def test_chain_eq1_report():
+    rep = {"chains": 1000, "n_steps": 20, "shape": "m16n8k8", "metric": "Eq. 1 relative L2 error vs CPU FP32 chain",
+           "results": {}}
+    for fmt in ("tf32", "bf16", "f16"):
+        for init in ("low", "fp32"):
+            _, _, Ds, a32, b32 = _run(fmt, 1000, 20, init, seed=0)
+            Dl = Ds.cpu().numpy().astype(np.float64)
+            D32 = O.chain_fp32(a32.numpy(), b32.numpy()).astype(np.float64)
+            with np.errstate(over="ignore", invalid="ignore"):
+                e = _eq1(Dl, D32)                         # (chains, N)
+            fin = np.isfinite(e)
+            rep["results"][f"{fmt}/init_{init}"] = {
+                "mean_rel_err": [float(e[fin[:, n], n].mean()) if fin[:, n].any() else None for n in range(20)],
+                "chains_overflowed": [int((~fin[:, n]).sum()) for n in range(20)]}
+    r = rep["results"]
+    # the paper's observations, asserted where they are properties of the
+    # arithmetic rather than of A100: BF16 (7-bit mantissa) errs more than TF32 (10-bit); init FP32
+    # adds conversion error; with low-precision init a length-1 chain is ~exact (one MMA of
+    # representable inputs, FP32 output).
+    assert r["bf16/init_low"]["mean_rel_err"][19] > 4 * r["tf32/init_low"]["mean_rel_err"][19]
+    for fmt in ("tf32", "bf16", "f16"):
+        assert r[f"{fmt}/init_low"]["mean_rel_err"][0] < 1e-6
+        assert r[f"{fmt}/init_fp32"]["mean_rel_err"][0] > r[f"{fmt}/init_low"]["mean_rel_err"][0]
+    out = os.environ.get("TCX_REPORT_DIR", "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, "chain_matmul_report.json"), "w") as f:
+        json.dump(rep, f, indent=1)

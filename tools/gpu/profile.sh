@@ -4,12 +4,12 @@ mkdir -p gpurun_out
 TAG=${1:-r01}
 BENCH="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
 $BENCH > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm_|tiles|sp24|fill_c" --csv \
     --log-file gpurun_out/${TAG}_launches.csv $BENCH > gpurun_out/ncu_launch.log 2>&1
 echo launches=$?
 for cfg in c3 c4 c5 c1 c3tf32; do
   case $cfg in
-    c3) K="regex:gemm_dense_kernel<2, 0>";; c3tf32) K="regex:gemm_dense_kernel<2, 1>";; c4) K="regex:gemm_dense_kernel<2, 2>";;
+    c3|c3tf32|c4) K="regex:gemm_dense";;
     c5) K="regex:gemm_sp24";; c1) K="regex:tiles16";;
   esac
   python tools/prof_kernels.py $cfg 2 > gpurun_out/plain_$cfg.log 2>&1 && \
