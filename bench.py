@@ -50,7 +50,7 @@ def peaks():
 
 # nominal dense ratios vs bf16 (B200_PROFILING.md nominal table: tf32 1.1 vs 2.25; int8 = fp8 rate 4.5;
 # 2:4 sparse doubles the dense rate): peak for kind = measured bf16 peak x ratio
-KIND_RATIO = {"bf16": 1.0, "f16": 1.0, "tf32": 0.5, "s8": 2.0, "sp16": 2.0}
+KIND_RATIO = {"bf16": 1.0, "f16": 1.0, "tf32": 0.5, "s8": 2.0, "sp16": 2.0, "sp8": 4.0, "sptf32": 1.0}
 
 
 class ClockSampler:
@@ -176,6 +176,33 @@ class Work:
             self.kernel = "gemm_sp24_kernel"
             self.step = lambda: tcx.gemm_sp24(self.vals, self.meta_hw, self.B, self.C, self.D)
             self.unit, self.bound = "TFLOP/s", "tensor"
+        elif cfg in ("c4sp", "c3sptf32"):   # NEXT-1: INT8 2:4 at C4's shape, TF32 1:2 at C3's shape
+            M = N = K = 16384 if cfg == "c4sp" else 8192
+            self.kind = "sp8" if cfg == "c4sp" else "sptf32"
+            self.shape = (M, N, K)
+            m0, m1 = self._rows(M)
+            if cfg == "c4sp":
+                vals, meta = g.sp24_problem_i8(M, K, seed, dev)
+                self.B = self._bcast(lambda: g.int8_matrix((N, K), seed, g.STREAM_B, dev))
+                self.C = g.int32_matrix((M, N), seed, g.STREAM_C, device=dev)[m0:m1].contiguous()
+                self.D = torch.empty(m1 - m0, N, dtype=torch.int32, device=dev)
+                ab, esize = tcx.S8, 1
+            else:
+                vals, meta = g.sp12_problem_tf32(M, K, seed, dev)
+                self.B = self._bcast(lambda: g.normal_matrix((N, K), "tf32", seed, g.STREAM_B, dev))
+                self.C = torch.zeros(m1 - m0, N, dtype=torch.float32, device=dev)
+                self.D = torch.empty(m1 - m0, N, dtype=torch.float32, device=dev)
+                ab, esize = tcx.TF32, 4
+            self.vals = vals[m0:m1].contiguous()
+            self.meta_hw = tcx.sp24_pack_meta(meta[m0:m1].contiguous(), m1 - m0, K, ab=ab)
+            del vals, meta
+            self.flops = 2.0 * (m1 - m0) * N * K          # dense-equivalent (DESIGN.md R-C13)
+            self.alg_bytes = (self.vals.numel() * esize + self.meta_hw.numel() + self.B.numel() * esize
+                              + 8 * (m1 - m0) * N)
+            self.kernel = "gemm_sp24_kernel<2,%s>" % ("i8" if cfg == "c4sp" else "tf32")
+            tf = cfg == "c3sptf32"
+            self.step = lambda: tcx.gemm_sp24(self.vals, self.meta_hw, self.B, self.C, self.D, tf32=tf)
+            self.unit, self.bound = ("TOPS" if cfg == "c4sp" else "TFLOP/s"), "tensor"
         elif cfg == "c1":
             count = 4096
             self.kind = "f16"
@@ -234,7 +261,7 @@ class Work:
             self.hA = self.As[0].cpu().pin_memory(); self.hB = self.Bs[0].cpu().pin_memory()
             self.hC = self.Cs[0].cpu().pin_memory(); self.hD = torch.empty_like(self.Ds[0], device="cpu").pin_memory()
             ins = [self.hA, self.hB, self.hC]
-        elif self.cfg == "c5":
+        elif hasattr(self, "vals"):                     # sparse configs
             self.hA = self.vals.cpu().pin_memory(); self.hM = self.meta_hw.cpu().pin_memory()
             self.hB = self.B.cpu().pin_memory(); self.hC = self.C.cpu().pin_memory()
             self.hD = torch.empty_like(self.D, device="cpu").pin_memory()
@@ -252,10 +279,10 @@ class Work:
             A = self.hA.to(self.dev, non_blocking=True); B = self.hB.to(self.dev, non_blocking=True)
             C = self.hC.to(self.dev, non_blocking=True)
             D = tcx.mma_tiles(A, B, C)
-        elif self.cfg == "c5":
+        elif hasattr(self, "vals"):
             A = self.hA.to(self.dev, non_blocking=True); Mh = self.hM.to(self.dev, non_blocking=True)
             B = self.hB.to(self.dev, non_blocking=True); C = self.hC.to(self.dev, non_blocking=True)
-            D = tcx.gemm_sp24(A, Mh, B, C)
+            D = tcx.gemm_sp24(A, Mh, B, C, tf32=(self.cfg == "c3sptf32"))
         else:
             A = self.hA.to(self.dev, non_blocking=True); B = self.hB.to(self.dev, non_blocking=True)
             C = self.hC.to(self.dev, non_blocking=True)
@@ -461,7 +488,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="tcx", choices=["tcx", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c3", "c3tf32", "c4", "c5", "c1"])
+    ap.add_argument("--config", default="c3", choices=["c3", "c3tf32", "c4", "c5", "c1", "c4sp", "c3sptf32"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -475,7 +502,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg_names = {"c3": "dense BF16 GEMM M=N=K=8192 (configs[2])", "c3tf32": "dense TF32 GEMM M=N=K=8192 (configs[2])",
                  "c4": "INT8 GEMM M=N=K=16384 (configs[3])", "c5": "2:4 sparse FP16 GEMM M=65536 N=K=16384 (configs[4])",
-                 "c1": "4096 m16n8k16 FP16 tiles (configs[0])"}
+                 "c1": "4096 m16n8k16 FP16 tiles (configs[0])",
+                 "c4sp": "INT8 2:4 sparse GEMM M=N=K=16384 (NEXT-1 at configs[3]'s shape)",
+                 "c3sptf32": "TF32 1:2 sparse GEMM M=N=K=8192 (NEXT-1 at configs[2]'s shape)"}
     metric = "dense & 2:4-sparse MMA TFLOP/s (INT8 TOPS) per B200, % of tensor-core peak"
 
     if args.impl == "reference":
@@ -532,7 +561,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None,
-            "dtype": {"c3": "bf16", "c3tf32": "tf32", "c4": "s8", "c5": "f16", "c1": "f16"}[args.config],
+            "dtype": {"c3": "bf16", "c3tf32": "tf32", "c4": "s8", "c5": "f16", "c1": "f16", "c4sp": "s8",
+                      "c3sptf32": "tf32"}[args.config],
             "data": "synthetic (seeded SplitMix64 / Box-Muller, tcxgen; generated on device)",
             "config": {"workload": cfg_names[args.config], "shape": list(work.shape),
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
@@ -542,7 +572,7 @@ def main():
             "e2e": e2e}
     if rank == 0 and world == 1 and not args.no_extras and args.config == "c3":
         also = {}
-        for extra in ("c3tf32", "c4", "c5", "c1"):
+        for extra in ("c3tf32", "c4", "c5", "c1", "c4sp", "c3sptf32"):
             try:
                 w2 = Work(extra, 0, 1, dev)
                 sampler.samples = []

@@ -64,6 +64,7 @@ def lib():
         L.tcxref_gemm_samples.restype = i32
         L.tcxref_sp24_expand.argtypes = [i32, i64, i64, vp, i64, vp, vp, i64]; L.tcxref_sp24_expand.restype = i64
         L.tcxref_sp24_compress.argtypes = [i32, i64, i64, vp, i64, vp, i64, vp]; L.tcxref_sp24_compress.restype = i64
+        L.tcxref_sp12_compress.argtypes = [i64, i64, vp, i64, vp, i64, vp]; L.tcxref_sp12_compress.restype = i64
         L.tcxref_tiles.argtypes = [i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]; L.tcxref_tiles.restype = i32
         L.tcxref_tiles2.argtypes = [i32, i32, i32, i32, i32, i64, vp, vp, vp, vp, vp]; L.tcxref_tiles2.restype = i32
         L.tcxref_model_dot.argtypes = [i32, i32, vp, vp, u32, i32, i32, i32, i32, i32, i32]
@@ -192,6 +193,17 @@ def sp24_compress(dense: np.ndarray):
     vals = np.zeros((M, K // 2), dtype=dense.dtype)
     meta = np.zeros((M, K // 32), dtype=np.uint32)
     bad = lib().tcxref_sp24_compress(dense.itemsize, M, K, _p(dense), K, _p(vals), K // 2, _p(meta))
+    return vals, meta, int(bad)
+
+
+def sp12_compress(dense: np.ndarray):
+    """TF32 1:2 compress (FP32-container bits, M x K): one kept element per aligned pair; returns
+    (vals M x K/2, canonical meta M x K/32, first violation row*G+group or -1)."""
+    dense = _c(dense, np.uint32)
+    M, K = dense.shape
+    vals = np.zeros((M, K // 2), dtype=np.uint32)
+    meta = np.zeros((M, K // 32), dtype=np.uint32)
+    bad = lib().tcxref_sp12_compress(M, K, _p(dense), K, _p(vals), K // 2, _p(meta))
     return vals, meta, int(bad)
 
 

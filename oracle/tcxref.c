@@ -487,6 +487,31 @@ int64_t tcxref_sp24_compress(int esize, int64_t M, int64_t K, const void *dense,
   return -1;
 }
 
+/* TF32 sparsity is 1:2 in hardware (DESIGN.md R-C12: the paper lists TF32 mma.sp shapes,
+   PAPER.md:619-620, without the rule): every aligned PAIR along K keeps one element — its nonzero,
+   or its lower element when both are zero; a pair with two nonzeros is a violation.  The kept
+   pair positions are written in the canonical 2:4 nibble (i0 in {0,1}, i1 in {2,3}).
+   returns -1 on success, else the first violating row*G + group (G = K/4, row-major order). */
+int64_t tcxref_sp12_compress(int64_t M, int64_t K, const uint32_t *dense, int64_t lda, uint32_t *vals,
+                             int64_t ld_vals, uint32_t *meta) {
+  int64_t i, g, G = K / 4;
+  memset(meta, 0, (size_t)(M * (K / 32)) * sizeof(uint32_t));
+  for (i = 0; i < M; i++) {
+    const uint32_t *d = dense + i * lda;
+    for (g = 0; g < G; g++) {
+      int nz[4], p, i0, i1;
+      for (p = 0; p < 4; p++) nz[p] = is_nonzero(4, (const char *)&d[4 * g + p]);
+      if ((nz[0] && nz[1]) || (nz[2] && nz[3])) return i * G + g;
+      i0 = (nz[1] && !nz[0]) ? 1 : 0;
+      i1 = (nz[3] && !nz[2]) ? 3 : 2;
+      vals[i * ld_vals + 2 * g] = d[4 * g + i0];
+      vals[i * ld_vals + 2 * g + 1] = d[4 * g + i1];
+      meta[i * (K / 32) + g / 8] |= (uint32_t)(i0 | (i1 << 2)) << (4 * (g % 8));
+    }
+  }
+  return -1;
+}
+
 /* ------------------------------------------------------------------------------------ */
 /* tile batch (tcx_mma_tiles semantics): D_t = A_t B_t + C_t, t < count.                   */
 /* A_t: m x k row-major, B_t: n x k ("col"), C_t/D_t: m x n row-major.                      */

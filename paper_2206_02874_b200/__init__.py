@@ -185,11 +185,12 @@ def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0):
 
 
 # ---------------------------------------------------------------------------------------- sparse
-def sp24_compress(A_dense):
+def sp24_compress(A_dense, tf32=False):
     """dense (M, K) 2:4 matrix -> (vals (M, K/2), meta_canon (M, K/32) int32).
-    Raises ValueError naming the first (row, group) with more than 2 nonzeros."""
+    Raises ValueError naming the first (row, group) with more than 2 nonzeros.  tf32=True (FP32
+    storage): the hardware's 1:2 rule — one element kept per aligned pair."""
     _dev_check(A_dense)
-    ab = ab_code(A_dense)
+    ab = ab_code(A_dense, tf32)
     M, K = A_dense.shape
     vals = torch.empty((M, K // 2), dtype=A_dense.dtype, device=A_dense.device)
     meta = torch.empty((M, K // 32), dtype=torch.int32, device=A_dense.device)
@@ -219,16 +220,18 @@ def sp24_pack_meta(meta_canon, M, K, ab=F16, check=True):
     return hw
 
 
-def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m=0):
-    """D = expand(vals, meta) x B + C; vals (M, K/2), B (N, K)."""
+def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m=0, tf32=False):
+    """D = expand(vals, meta) x B + C; vals (M, K/2), B (N, K).  FP16/BF16 -> FP32, INT8 -> INT32
+    (meta_hw packed with the same ab: sp24_pack_meta(meta, M, K, ab=S8) for int8)."""
     _dev_check(vals, meta_hw, B, C, D)
-    ab = ab_code(vals)
+    ab = ab_code(vals, tf32)
     M = vals.shape[0]
     N, K = B.shape
+    cd = S32 if ab == S8 else F32
     if D is None:
-        D = torch.empty((M, N), dtype=torch.float32, device=vals.device)
+        D = torch.empty((M, N), dtype=torch.int32 if cd == S32 else torch.float32, device=vals.device)
     opts = GemmOpts(cta_group, max_ctas, group_m)
-    _check(lib().tcx_gemm_sp24_ex(ab, F32, M, N, K, _ptr(vals), vals.stride(0), _ptr(meta_hw), _ptr(B), B.stride(0),
+    _check(lib().tcx_gemm_sp24_ex(ab, cd, M, N, K, _ptr(vals), vals.stride(0), _ptr(meta_hw), _ptr(B), B.stride(0),
                                   _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
                                   ctypes.byref(opts), _stream(vals)))
     return D

@@ -211,7 +211,7 @@ tcx_status tcx_gemm(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
 tcx_status tcx_sp24_compress(tcx_dtype ab, int64_t M, int64_t K, const void* A_dense, int64_t lda, void* A_vals,
                              uint32_t* meta_canon, int64_t* d_first_bad, void* stream) {
   const int es = esize_of(ab);
-  if (!(ab == TCX_F16 || ab == TCX_BF16 || ab == TCX_S8))
+  if (!(ab == TCX_F16 || ab == TCX_BF16 || ab == TCX_S8 || ab == TCX_TF32))
     return set_error(TCX_ERR_UNSUPPORTED, "tcx_sp24_compress: ab=%d", ab);
   if (M < 0 || K < 0 || K % 32) return set_error(TCX_ERR_INVALID_VALUE, "tcx_sp24_compress: K must be a multiple of 32");
   if (lda < K) return set_error(TCX_ERR_INVALID_VALUE, "tcx_sp24_compress: lda < K");
@@ -222,25 +222,27 @@ tcx_status tcx_sp24_compress(tcx_dtype ab, int64_t M, int64_t K, const void* A_d
   DevInfo dev;
   tcx_status st = current_device(&dev);
   if (st != TCX_OK) return st;
-  return launch_sp24_compress(es, M, K, A_dense, lda, A_vals, meta_canon, d_first_bad, (cudaStream_t)stream);
+  return launch_sp24_compress(es, ab == TCX_TF32, M, K, A_dense, lda, A_vals, meta_canon, d_first_bad,
+                              (cudaStream_t)stream);
 }
 
 size_t tcx_sp24_meta_hw_bytes(tcx_dtype ab, int64_t M, int64_t K) {
-  if (!(ab == TCX_F16 || ab == TCX_BF16) || M < 0 || K < 0) return 0;
-  return (size_t)(M * K / 8);
+  if (!(ab == TCX_F16 || ab == TCX_BF16 || ab == TCX_S8 || ab == TCX_TF32) || M < 0 || K < 0) return 0;
+  return (size_t)(M * K / (ab == TCX_TF32 ? 4 : 8));
 }
 
 tcx_status tcx_sp24_pack_meta(tcx_dtype ab, int64_t M, int64_t K, const uint32_t* meta_canon, void* meta_hw,
                               int64_t* d_first_bad, void* stream) {
-  if (!(ab == TCX_F16 || ab == TCX_BF16)) return set_error(TCX_ERR_UNSUPPORTED, "tcx_sp24_pack_meta: ab=%d", ab);
-  if (M < 0 || K < 0 || M % 128 || K % 128)
-    return set_error(TCX_ERR_UNSUPPORTED, "tcx_sp24_pack_meta: M and K must be multiples of 128");
+  if (!(ab == TCX_F16 || ab == TCX_BF16 || ab == TCX_S8 || ab == TCX_TF32))
+    return set_error(TCX_ERR_UNSUPPORTED, "tcx_sp24_pack_meta: ab=%d", ab);
+  if (M < 0 || K < 0 || M % 128 || K % (ab == TCX_TF32 ? 64 : 128))
+    return set_error(TCX_ERR_UNSUPPORTED, "tcx_sp24_pack_meta: M %% 128 and K %% %d must be 0", ab == TCX_TF32 ? 64 : 128);
   if (!d_first_bad) return set_error(TCX_ERR_INVALID_VALUE, "tcx_sp24_pack_meta: d_first_bad is NULL");
   if (M > 0 && K > 0 && (!meta_canon || !meta_hw)) return set_error(TCX_ERR_INVALID_VALUE, "tcx_sp24_pack_meta: NULL operand");
   DevInfo dev;
   tcx_status st = current_device(&dev);
   if (st != TCX_OK) return st;
-  return launch_sp24_pack(M, K, meta_canon, meta_hw, d_first_bad, (cudaStream_t)stream);
+  return launch_sp24_pack(ab, M, K, meta_canon, meta_hw, d_first_bad, (cudaStream_t)stream);
 }
 
 tcx_status tcx_gemm_sp24(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K, const void* A_vals,
@@ -252,12 +254,14 @@ tcx_status tcx_gemm_sp24(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64
 tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K, const void* A_vals,
                             int64_t lda_vals, const void* meta_hw, const void* B, int64_t ldb, const void* C,
                             int64_t ldc, void* D, int64_t ldd, const tcx_gemm_opts* opts, void* stream) {
-  if (!((ab == TCX_F16 || ab == TCX_BF16) && cd == TCX_F32))
-    return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: (ab=%d, cd=%d) not supported (NEXT: bf16/i8/tf32 variants)", ab, cd);
+  if (!(((ab == TCX_F16 || ab == TCX_BF16 || ab == TCX_TF32) && cd == TCX_F32) || (ab == TCX_S8 && cd == TCX_S32)))
+    return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: (ab=%d, cd=%d) not supported", ab, cd);
   if (M < 0 || N < 0 || K < 0) return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm_sp24: negative size");
   if (M == 0 || N == 0) return TCX_OK;
-  if (M % 128 || K % 128 || N % 16 || K == 0)
-    return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: requires M %% 128 == 0, K %% 128 == 0, N %% 16 == 0");
+  const int64_t kstage = ab == TCX_S8 ? 256 : ab == TCX_TF32 ? 64 : 128;
+  if (M % 128 || K % kstage || N % 16 || K == 0)
+    return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: requires M %% 128 == 0, K %% %d == 0, N %% 16 == 0",
+                     (int)kstage);
   tcx_status st = check_gemm_common("tcx_gemm_sp24", ab, cd, M, N, K, A_vals, lda_vals, B, ldb, C, ldc, D, ldd, K / 2);
   if (st != TCX_OK) return st;
   if (!meta_hw || !aligned16(meta_hw)) return set_error(TCX_ERR_MISALIGNED, "tcx_gemm_sp24: meta_hw NULL or misaligned");

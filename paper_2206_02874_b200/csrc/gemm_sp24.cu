@@ -8,6 +8,12 @@
 // tcgen05.cp 128x128b, then issues 4 x tcgen05.mma.sp.kind::f16 (logical K = 32 each).
 // TMEM: two 240-column FP32 accumulators (cols 0 and 256) + a 4-slot metadata ring (cols 496..511),
 // so the epilogue of tile t overlaps the MMAs of tile t+1 (UMMA N = 240: 2 x 240 + 16 <= 512).
+// KIND_I8 (2:4 on bytes, S32 accumulate, wrap): a stage is 256 logical K (sA 128 B/row, B two
+// 128-byte boxes, metadata two 2 KiB atoms copied by two 128x128b tcgen05.cp into 8 columns), and
+// each of the 4 tcgen05.mma.sp.kind::i8 (logical K = 64) reads 2 metadata columns; the ring is
+// 4 x 8 columns at 480..511 and the accumulators sit at 0 and 240.
+// KIND_TF32 (hardware 1:2 sparsity, logical K = 16 per MMA): a stage is 64 logical K (32 kept TF32 =
+// 128 B of sA per row), B two 32-element boxes, one metadata atom; layout as kind::f16 over 2K.
 // "The hardware selector determines which values should participate ... on the fly":
 // the MMA skips the zero products; throughput doubles at the same latency.
 #include "tcx_internal.h"
@@ -18,25 +24,32 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BN = 240;            // UMMA N
-constexpr int ACC_STRIDE = 256;    // TMEM column offset between the two accumulators
-constexpr int META_COL = 496;      // metadata ring: 4 slots x 4 columns
 constexpr int NUM_THREADS = 256;
 constexpr int EPI_WARPS = 4;
 constexpr int GROUP_M = 8;            // default raster group (cluster-tile rows sweeping N together)
-constexpr int KL = 128;            // logical K per stage
-constexpr int META_BYTES = 2048;   // one 128-row x 128-logical-K metadata atom
-
-template <int CG>
+template <int CG, int KIND>
 struct SpCfg {
+  static constexpr int ES = KIND == KIND_I8 ? 1 : KIND == KIND_TF32 ? 4 : 2;   // element bytes
+  static constexpr int KL = 256 / ES;                      // logical K per stage (= 128 B of kept A)
+  static constexpr int BOX = 128 / ES;                     // elements per 128-byte SW128 box row
+  // 2 KiB metadata atoms per stage (one atom = 128 rows x 128 logical 8/16-bit K; a TF32 element
+  // counts as two 16-bit halves, so a 64-logical-K TF32 stage is one atom)
+  static constexpr int META_ATOMS = KIND == KIND_TF32 ? 1 : KL / 128;
+  static constexpr int META_BYTES = 2048 * META_ATOMS;
+  static constexpr int META_COLS = 4 * META_ATOMS;         // TMEM columns per stage
+  static constexpr int MMA_COLS = META_COLS / 4;           // metadata columns read by one MMA
   static constexpr int BN_LOAD = BN / CG;
-  static constexpr int A_BYTES = BM * 128;                 // 64 kept fp16 per row
-  static constexpr int B_HALF = BN_LOAD * 128;             // one 64-element SW128 box
+  static constexpr int A_BYTES = BM * 128;                 // 128 bytes of kept values per row
+  static constexpr int B_HALF = BN_LOAD * 128;             // one SW128 box (128 bytes of K per row)
   static constexpr int B_BYTES = 2 * B_HALF;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + META_BYTES;
   static constexpr int STAGES = CG == 1 ? 2 : 4;
   static constexpr int SMEM_DATA = STAGES * STAGE_BYTES;
   static constexpr int SMEM_TOTAL = SMEM_DATA + 1024 + 1024;
+  static constexpr int META_COL = 512 - STAGES * META_COLS;    // metadata ring at the top of TMEM
+  static constexpr int ACC_STRIDE = KIND == KIND_I8 ? BN : 256;   // second accumulator's column
   static_assert(B_HALF % 1024 == 0, "SW128 atoms need 1 KiB alignment");
+  static_assert(ACC_STRIDE + BN <= META_COL, "TMEM budget");
 };
 
 struct Smem {
@@ -58,13 +71,14 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64
   nt = r / gm;
 }
 
-template <int CG>
+template <int CG, int KIND>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmE, int64_t M, int64_t N, int64_t K,
-                 const float* __restrict__ Cptr, int64_t ldc, float* __restrict__ Dptr, int64_t ldd, uint32_t idesc,
+                 const uint32_t* __restrict__ Cptr, int64_t ldc, uint32_t* __restrict__ Dptr, int64_t ldd, uint32_t idesc,
                  int group_m) {
-  using C_ = SpCfg<CG>;
+  using C_ = SpCfg<CG, KIND>;
+  constexpr int KL = C_::KL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem* sm = (Smem*)(smem + C_::SMEM_DATA);
@@ -106,21 +120,21 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           uint8_t* sa = smem + stage * C_::STAGE_BYTES;
           uint8_t* sb = sa + C_::A_BYTES;
           uint8_t* se = sb + C_::B_BYTES;
-          const int ka = (int)(kb * 64);           // kept-value column
+          const int ka = (int)(kb * (KL / 2));     // kept-value column
           const int kx = (int)(kb * KL);           // logical column of B
-          const int erow = (int)((mb * k_blocks + kb) * 16);
+          const int erow = (int)((mb * k_blocks + kb) * 16 * C_::META_ATOMS);
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&sm->full[stage], C_::STAGE_BYTES);
             tma_load_2d(sa, &tmA, &sm->full[stage], ka, (int)mrow);
             tma_load_2d(sb, &tmB, &sm->full[stage], kx, brow);
-            tma_load_2d(sb + C_::B_HALF, &tmB, &sm->full[stage], kx + 64, brow);
+            tma_load_2d(sb + C_::B_HALF, &tmB, &sm->full[stage], kx + C_::BOX, brow);
             tma_load_2d(se, &tmE, &sm->full[stage], 0, erow);
           } else {
             if (leader) mbar_arrive_expect_tx(&sm->full[stage], 2 * C_::STAGE_BYTES);
             const uint32_t bar = full0_cluster + stage * 8;
             tma_load_2d_cg2(sa, &tmA, bar, ka, (int)mrow);
             tma_load_2d_cg2(sb, &tmB, bar, kx, brow);
-            tma_load_2d_cg2(sb + C_::B_HALF, &tmB, bar, kx + 64, brow);
+            tma_load_2d_cg2(sb + C_::B_HALF, &tmB, bar, kx + C_::BOX, brow);
             tma_load_2d_cg2(se, &tmE, bar, 0, erow);
           }
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
@@ -135,7 +149,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if constexpr (CG == 2) mbar_wait_cluster(&sm->tmem_empty[acc], acc_phase ^ 1);
         else mbar_wait(&sm->tmem_empty[acc], acc_phase ^ 1);
         tc05_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * ACC_STRIDE;
+        const uint32_t tmem_d = tmem_base + acc * C_::ACC_STRIDE;
         for (int64_t kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&sm->full[stage], phase);
           tc05_fence_after();
@@ -143,15 +157,22 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const uint32_t sa = smem_u32(smem + stage * C_::STAGE_BYTES);
             const uint32_t sb = sa + C_::A_BYTES;
             const uint32_t se = sb + C_::B_BYTES;
-            const uint32_t tmeta = tmem_base + META_COL + stage * 4;
-            // metadata atom -> TMEM (128 lanes x 16 B); executes in order before the MMAs below
-            tc05_cp_128x128b<CG>(tmeta, sdesc(se, 128, 128, 0));
+            const uint32_t tmeta = tmem_base + C_::META_COL + stage * C_::META_COLS;
+            // metadata atoms -> TMEM (128 lanes x 16 B each); execute in order before the MMAs below
+#pragma unroll
+            for (int h = 0; h < C_::META_ATOMS; ++h) tc05_cp_128x128b<CG>(tmeta + 4 * h, sdesc(se + 2048 * h, 128, 128, 0));
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
+              // MMA j: 32 bytes of kept A (K/2 logical), 64 bytes of B (one half of a SW128 box row)
               const uint64_t ad = sdesc(sa + j * 32, 16, 1024, 2);
               const uint64_t bd = sdesc(sb + (j >> 1) * C_::B_HALF + (j & 1) * 64, 16, 1024, 2);
-              const uint32_t e = tmeta + j;
-              umma_sp<CG, KIND_F16>(tmem_d, ad, bd, e & ~1u, idesc | (e & 1u), (kb | j) ? 1u : 0u);
+              if constexpr (KIND == KIND_I8) {
+                const uint32_t e = tmeta + 2 * j;          // 2 columns per MMA, selector 0
+                umma_sp<CG, KIND_I8>(tmem_d, ad, bd, e, idesc, (kb | j) ? 1u : 0u);
+              } else {
+                const uint32_t e = tmeta + j;              // low address bit -> sparse selector
+                umma_sp<CG, KIND>(tmem_d, ad, bd, e & ~1u, idesc | (e & 1u), (kb | j) ? 1u : 0u);
+              }
             }
             tc05_commit<CG>(&sm->empty[stage]);
             if (kb == k_blocks - 1) tc05_commit<CG>(&sm->tmem_full[acc]);
@@ -179,7 +200,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       for (int ch = 0; ch < NCH; ++ch) {
         const int64_t c0 = col0 + ch * 16;
         uint32_t v[16];
-        tmem_ld_32x32b_x16(tmem_base + acc * ACC_STRIDE + ch * 16 + ((uint32_t)(e * 32) << 16), v);
+        tmem_ld_32x32b_x16(tmem_base + acc * C_::ACC_STRIDE + ch * 16 + ((uint32_t)(e * 32) << 16), v);
         uint32_t cv[16];
         const bool ok = c0 < N;          // N % 16 == 0: a chunk is all-in or all-out
         if (Cptr != nullptr && ok) {
@@ -199,8 +220,13 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if (ok) {
           uint4* drow = (uint4*)(Dptr + row * ldd + c0);
           if (Cptr != nullptr) {
+            if constexpr (KIND == KIND_I8) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__fadd_rn(__uint_as_float(v[j]), __uint_as_float(cv[j])));
+              for (int j = 0; j < 16; ++j) v[j] = v[j] + cv[j];       // S32: wrap mod 2^32
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__fadd_rn(__uint_as_float(v[j]), __uint_as_float(cv[j])));
+            }
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j) drow[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
@@ -215,23 +241,25 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (warp == 2) { tc05_fence_after(); tmem_dealloc<CG>(tmem_base, 512); }
 }
 
-template <int CG>
+template <int CG, int KIND>
 tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
-  using C_ = SpCfg<CG>;
+  using C_ = SpCfg<CG, KIND>;
   if (a.M % (BM * CG)) return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: M %% %d != 0", BM * CG);
-  const CUtensorMapDataType dt = a.ab == TCX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const CUtensorMapDataType dt = KIND == KIND_I8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : KIND == KIND_TF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : a.ab == TCX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tA, tB, tE;
-  tcx_status st = make_tmap_2d(&tA, dt, a.A, (uint64_t)(a.K / 2), (uint64_t)a.M, (uint64_t)(a.lda * 2), 64, BM,
+  tcx_status st = make_tmap_2d(&tA, dt, a.A, (uint64_t)(a.K / 2), (uint64_t)a.M, (uint64_t)(a.lda * C_::ES), C_::BOX, BM,
                                CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != TCX_OK) return st;
-  st = make_tmap_2d(&tB, dt, a.B, (uint64_t)a.K, (uint64_t)a.N, (uint64_t)(a.ldb * 2), 64, C_::BN_LOAD,
+  st = make_tmap_2d(&tB, dt, a.B, (uint64_t)a.K, (uint64_t)a.N, (uint64_t)(a.ldb * C_::ES), C_::BOX, C_::BN_LOAD,
                     CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != TCX_OK) return st;
-  const uint64_t meta_rows = (uint64_t)(a.M * a.K / 8) / 128;
-  st = make_tmap_2d(&tE, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.meta_hw, 128, meta_rows, 128, 128, 16,
+  const uint64_t meta_rows = (uint64_t)(a.M * a.K * (KIND == KIND_TF32 ? 2 : 1) / 8) / 128;
+  st = make_tmap_2d(&tE, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.meta_hw, 128, meta_rows, 128, 128, 16 * C_::META_ATOMS,
                     CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st != TCX_OK) return st;
-  auto kern = gemm_sp24_kernel<CG>;
+  auto kern = gemm_sp24_kernel<CG, KIND>;
   TCX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_TOTAL));
   const int64_t tiles = (a.M / (BM * CG)) * ((a.N + BN - 1) / BN);
   int64_t clusters = tiles;
@@ -247,12 +275,14 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr; cfg.numAttrs = 1;
-  // idesc: sparse flag [2], c F32 [4,6)=1, a/b format [7,10)/[10,13), N>>3 [17,23), M>>4 [24,29)
-  const uint32_t fmt = a.ab == TCX_BF16 ? 1u : 0u;
-  const uint32_t idesc = (1u << 2) | (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
+  // idesc: sparse flag [2], c format [4,6) (F32 = 1, S32 = 2), a/b format [7,10)/[10,13)
+  // (f16 0, bf16 1; s8 signed 1), N>>3 [17,23), M>>4 [24,29); saturate [3] = 0 (wrap)
+  const uint32_t fmt = KIND == KIND_TF32 ? 2u : (KIND == KIND_I8 || a.ab == TCX_BF16) ? 1u : 0u;
+  const uint32_t cfmt = KIND == KIND_I8 ? 2u : 1u;
+  const uint32_t idesc = (1u << 2) | (cfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
                          ((uint32_t)((BM * CG) >> 4) << 24);
-  TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tE, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K, (const float*)a.C,
-                                  (int64_t)a.ldc, (float*)a.D, (int64_t)a.ldd, idesc,
+  TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tE, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
+                                  (const uint32_t*)a.C, (int64_t)a.ldc, (uint32_t*)a.D, (int64_t)a.ldd, idesc,
                                   a.group_m > 0 ? a.group_m : GROUP_M));
   count_launch();
   return TCX_OK;
@@ -261,8 +291,9 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
 }  // namespace
 
 tcx_status launch_gemm_sp24(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
-  if (a.cta_group == 1) return launch_sp<1>(a, dev, s);
-  return launch_sp<2>(a, dev, s);
+  if (a.ab == TCX_S8) return a.cta_group == 1 ? launch_sp<1, KIND_I8>(a, dev, s) : launch_sp<2, KIND_I8>(a, dev, s);
+  if (a.ab == TCX_TF32) return a.cta_group == 1 ? launch_sp<1, KIND_TF32>(a, dev, s) : launch_sp<2, KIND_TF32>(a, dev, s);
+  return a.cta_group == 1 ? launch_sp<1, KIND_F16>(a, dev, s) : launch_sp<2, KIND_F16>(a, dev, s);
 }
 
 }  // namespace tcx

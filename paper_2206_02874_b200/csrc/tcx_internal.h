@@ -57,9 +57,9 @@ tcx_status launch_gemm_dense(const GemmArgs& a, const DevInfo& dev, cudaStream_t
 tcx_status launch_gemm_sp24(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);
 tcx_status launch_fill_c(const GemmArgs& a, cudaStream_t s);   // K == 0: D = C (or 0)
 
-tcx_status launch_sp24_compress(int esize, int64_t M, int64_t K, const void* A, int64_t lda,
+tcx_status launch_sp24_compress(int esize, bool pair, int64_t M, int64_t K, const void* A, int64_t lda,
                                 void* vals, uint32_t* meta, int64_t* d_bad, cudaStream_t s);
-tcx_status launch_sp24_pack(int64_t M, int64_t K, const uint32_t* meta, void* hw, int64_t* d_bad,
+tcx_status launch_sp24_pack(tcx_dtype ab, int64_t M, int64_t K, const uint32_t* meta, void* hw, int64_t* d_bad,
                             cudaStream_t s);
 tcx_status launch_round_tf32(const float* in, float* out, int64_t n, cudaStream_t s);
 tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_result* out);

@@ -202,6 +202,33 @@ def sp24_problem(M, K, seed, fmt="f16", device="cpu"):
     return vals, sp24_canonical_meta(pairs)
 
 
+def sp24_problem_i8(M, K, seed, device="cpu"):
+    """INT8 2:4 operand (NEXT-1 at C4's shape): pairs uniform over the 6, kept values uniform in
+    [-128, 127] without 0 (so every group has exactly 2 nonzeros)."""
+    pairs = sp24_pairs(M, K, seed, STREAM_POS, device)
+    v = int32_matrix((M, K // 2), seed, STREAM_SPVAL, -128, 126, device)
+    v = torch.where(v >= 0, v + 1, v)
+    return v.to(torch.int8), sp24_canonical_meta(pairs)
+
+
+def sp12_problem_tf32(M, K, seed, device="cpu"):
+    """TF32 1:2 operand (hardware TF32 sparsity, DESIGN.md R-C12): in every aligned pair one element
+    kept, position uniform; values N(0,1) rounded to TF32, never 0.  Canonical nibble per group of 4:
+    i0 in {0,1}, i1 in {2,3}.  Returns (vals (M, K/2) float32, meta (M, K/32) int32)."""
+    n = M * (K // 4)
+    pat = torch.empty(n, dtype=torch.uint8, device=device)
+
+    def fn(s, m):
+        z = splitmix(seed, STREAM_POS, torch.arange(s, s + m, dtype=torch.int64, device=device))
+        return torch.remainder(_srl(z, 32), 4).to(torch.uint8)
+    _fill(pat, fn)
+    # pattern p -> (i0, i1) = (p & 1, 2 + (p >> 1)) -> index into PAIRS
+    to_pair = torch.tensor([PAIRS.index((p & 1, 2 + (p >> 1))) for p in range(4)], dtype=torch.uint8, device=device)
+    pairs = to_pair[pat.long()].view(M, K // 4)
+    vals = normal_matrix((M, K // 2), "tf32", seed, STREAM_SPVAL, device, redraw_zero=True)
+    return vals, sp24_canonical_meta(pairs)
+
+
 # ----------------------------------------------------------------------------------------------
 # Config 2: crafted numeric-probe tiles (SURVEY §8(d) "The eight C2 crafted classes").
 # Each tile is m16n8k16 (TF32: k16 = two chained k8); only d00 is probed, the paper's placement

@@ -50,6 +50,20 @@ def test_sp24_golden():
             assert [float(v) for v in vals.view(np.float16)[0, :2]] == [float(v) for v in row[3].split(",")]
             nib = int(meta[0, 0]) & 0xF
             assert (nib & 3, nib >> 2) == tuple(map(int, row[5].split(",")))
+        elif row[0] in ("sp12", "sp12bad"):
+            g = np.array([float(v) for v in row[1].split(",")], np.float32)
+            dense = np.zeros((1, 32), np.float32)
+            dense[0, :4] = g
+            vals, meta, bad = O.sp12_compress(dense.view(np.uint32))
+            if row[0] == "sp12bad":
+                assert bad == 0
+                n += 1
+                continue
+            assert bad == -1
+            nib = int(meta[0, 0]) & 0xF
+            i0, i1 = map(int, row[3].split(","))
+            assert (nib & 3, nib >> 2) == (i0, i1)
+            assert list(vals.view(np.float32)[0, :2]) == [g[i0], g[i1]]
         elif row[0] == "word":
             g = [float(v) for v in row[1].split(",")]
             dense = np.zeros((1, 32), np.float16)
@@ -59,7 +73,7 @@ def test_sp24_golden():
             # groups 2..7 are all-zero -> padded (0,1) = 0x4 each
             assert int(meta[0, 0]) & 0xFF == int(row[2], 16)
         n += 1
-    assert n == 9
+    assert n == 15
 
 
 def test_sp24_reject_and_roundtrip():
@@ -87,6 +101,30 @@ def test_sp24_reject_and_roundtrip():
     d3[0, :4] = [-0.0, np.nan, 1.0, -0.0]
     _, meta3, bad = O.sp24_compress(d3.view(np.uint16))
     assert bad == -1 and int(meta3[0, 0]) & 0xF == (1 | (2 << 2))
+
+
+def test_sp12_roundtrip_and_first_violation():
+    """TF32 1:2: expand(compress(A)) == A for one-nonzero-per-pair matrices (SPEC.md:232 analogue);
+    the first pair with two nonzeros is reported in row-major order."""
+    rng = np.random.default_rng(12)
+    M, K = 9, 64
+    dense = np.zeros((M, K), np.float32)
+    pick = rng.integers(0, 2, (M, K // 2))
+    keep = rng.random((M, K // 2)) < 0.9
+    for i in range(M):
+        for q in range(K // 2):
+            if keep[i, q]:
+                dense[i, 2 * q + pick[i, q]] = rng.standard_normal() + 5
+    vals, meta, bad = O.sp12_compress(dense.view(np.uint32))
+    assert bad == -1
+    assert np.array_equal(O.sp24_expand(vals, meta, K), dense.view(np.uint32))
+    nib = np.array([[(meta[i, g // 8] >> (4 * (g % 8))) & 0xF for g in range(K // 4)] for i in range(M)])
+    assert np.all((nib & 3) <= 1) and np.all((nib >> 2) >= 2)
+    d2 = dense.copy()
+    d2[4, 10:12] = 1.0
+    d2[6, 0:2] = 1.0
+    _, _, bad = O.sp12_compress(d2.view(np.uint32))
+    assert bad == 4 * (K // 4) + 10 // 4
 
 
 def test_sparse_equals_dense_of_expanded():
