@@ -155,11 +155,20 @@ tcx_status tcx_round_tf32(const float* in, float* out, int64_t n, void* stream);
  *   TCX_PROBE_TC05         tcgen05.mma issued by one thread; ILP = independent accumulators
  *                          in flight per commit; `warps` = issuing CTAs per SM (1)
  *   TCX_PROBE_TC05_SP      tcgen05.mma.sp
+ * data-movement kinds (the paper's §VII; throughput in bytes/clk/SM, reported
+ * in fma_per_clk_per_sm):
+ *   TCX_PROBE_LDMATRIX     ldmatrix.sync.aligned.m8n8.x{m}[.trans if n].shared.b16, m in {1,2,4}
+ *                          (Table ldmatrix-summary)
+ *   TCX_PROBE_LDSHARED     ld.shared of m = 4 or 8 bytes per lane with an n-way bank conflict
+ *                          (lane l reads byte l*4*n; Table ldshared-latency)
+ *   TCX_PROBE_TMEM_LD      tcgen05.ld.sync.aligned.32x32b.x{m} + tcgen05.wait::ld, m in
+ *                          {1,2,4,8,16,32}: B200's accumulator read-out (warps <= 16)
  * Synchronous; allocates and frees its own scratch.  Shapes not implemented ->
  * TCX_ERR_UNSUPPORTED.
  * ------------------------------------------------------------------------------------- */
 typedef enum { TCX_PROBE_MMA_SYNC = 0, TCX_PROBE_MMA_SP_SYNC = 1, TCX_PROBE_TC05 = 2,
-               TCX_PROBE_TC05_SP = 3 } tcx_probe_kind;
+               TCX_PROBE_TC05_SP = 3, TCX_PROBE_LDMATRIX = 4, TCX_PROBE_LDSHARED = 5,
+               TCX_PROBE_TMEM_LD = 6 } tcx_probe_kind;
 typedef struct {
   int kind;          /* tcx_probe_kind */
   int ab, cd;        /* tcx_dtype */
@@ -181,6 +190,14 @@ typedef struct {
   uint32_t sink;                  /* data-dependence sink (keeps the MMAs alive) */
 } tcx_probe_result;
 tcx_status tcx_probe(int device, const tcx_probe_config* cfg, tcx_probe_result* out);
+
+/* tcx_ldmatrix_dump — one ldmatrix.sync.aligned.m8n8.x{num}[.trans].shared.b16 by one warp, for
+ * checking the fragments it delivers against the instruction's definition (PAPER.md:685-700,
+ * Fig. func_ldmatrix): src (device) = 512 b16 elements copied to shared memory; row_elem (device,
+ * 32 ints) = the element offset of the 16-byte row lane l addresses (lanes >= 8*num ignored);
+ * out (device, 32*num u32) = register j of lane l at out[l*num + j].  Asynchronous. */
+tcx_status tcx_ldmatrix_dump(int num, int trans, const void* src, const int32_t* row_elem, uint32_t* out,
+                             void* stream);
 
 /* numeric probe through tcgen05: the same tile batch as tcx_mma_tiles (F16/BF16 m16n8k16,
  * TF32 m16n8k8|16), but each group of 8 tiles is packed block-diagonally into one

@@ -254,3 +254,25 @@ def chain_fp32(A0: np.ndarray, Bs: np.ndarray) -> np.ndarray:
     Ds = np.zeros((count, n_steps, 16, 8), dtype=np.float32)
     lib().tcxref_chain_fp32(count, n_steps, _p(A0), _p(Bs), _p(Ds))
     return Ds
+
+
+# ---------------------------------------------------------------------------- ldmatrix (NEXT-3)
+def ldmatrix(num: int, trans: bool, smem_u16: np.ndarray, row_elem: np.ndarray) -> np.ndarray:
+    """The fragments one warp receives from ldmatrix.sync.aligned.m8n8.x{num}[.trans].shared.b16
+    (Fig. func_ldmatrix: "it loads N x 128 bytes per warp ... each thread stores
+    N x 4 bytes"; "If N = 4, then every thread will provide a valid p ... (e.g. T0 - T7 for N = 1)").
+    Matrix j (j < num) is 8 rows x 8 b16 elements; its row r starts at element row_elem[8j + r].
+    Lane l's register j holds two b16 (first in the low half):
+      non-trans: M_j[l // 4][2 (l % 4)], M_j[l // 4][2 (l % 4) + 1]
+      trans:     M_j[2 (l % 4)][l // 4], M_j[2 (l % 4) + 1][l // 4]
+    (the register layout the paper says matches the mma operand arrangement).
+    Plain Python loops (32 lanes x num registers).  Returns (32, num) uint32."""
+    smem = np.asarray(smem_u16, dtype=np.uint16)
+    out = np.zeros((32, num), dtype=np.uint32)
+    for j in range(num):
+        M = [[int(smem[int(row_elem[8 * j + r]) + c]) for c in range(8)] for r in range(8)]
+        for l in range(32):
+            g, t = l // 4, l % 4
+            lo, hi = (M[g][2 * t], M[g][2 * t + 1]) if not trans else (M[2 * t][g], M[2 * t + 1][g])
+            out[l, j] = lo | (hi << 16)
+    return out

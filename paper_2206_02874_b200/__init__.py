@@ -31,7 +31,7 @@ _STATUS = {0: "TCX_OK", 1: "TCX_ERR_INVALID_VALUE", 2: "TCX_ERR_UNSUPPORTED", 3:
 
 EXPORTS = ["tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_mma_chain", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
            "tcx_sp24_meta_hw_bytes", "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_gemm_sp24_ex", "tcx_round_tf32",
-           "tcx_probe",
+           "tcx_probe", "tcx_ldmatrix_dump",
            "tcx_status_string", "tcx_last_error", "tcx_version", "tcx_launch_count"]
 
 
@@ -84,12 +84,13 @@ def lib():
                                    ctypes.POINTER(GemmOpts), vp]
     L.tcx_round_tf32.argtypes = [vp, vp, i64, vp]
     L.tcx_probe.argtypes = [i32, ctypes.POINTER(ProbeConfig), ctypes.POINTER(ProbeResult)]
+    L.tcx_ldmatrix_dump.argtypes = [i32, i32, vp, vp, vp, vp]
     L.tcx_status_string.restype = ctypes.c_char_p
     L.tcx_last_error.restype = ctypes.c_char_p
     L.tcx_version.restype = ctypes.c_char_p
     L.tcx_launch_count.restype = ctypes.c_uint64
     for f in ("tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_mma_chain", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
-              "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_gemm_sp24_ex", "tcx_round_tf32", "tcx_probe"):
+              "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_gemm_sp24_ex", "tcx_round_tf32", "tcx_probe", "tcx_ldmatrix_dump"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -246,7 +247,8 @@ def round_tf32(x, out=None):
 
 
 # ---------------------------------------------------------------------------------------- probe
-PROBE_KINDS = {"mma_sync": 0, "mma_sp_sync": 1, "tc05": 2, "tc05_sp": 3}
+PROBE_KINDS = {"mma_sync": 0, "mma_sp_sync": 1, "tc05": 2, "tc05_sp": 3, "ldmatrix": 4, "ld_shared": 5,
+               "tmem_ld": 6}
 
 
 def probe(kind="mma_sync", ab=F16, cd=F32, m=16, n=8, k=16, cta_group=1, warps=1, ilp=1, iters=1024,
@@ -256,3 +258,12 @@ def probe(kind="mma_sync", ab=F16, cd=F32, m=16, n=8, k=16, cta_group=1, warps=1
     res = ProbeResult()
     _check(lib().tcx_probe(device, ctypes.byref(cfg), ctypes.byref(res)))
     return {f: getattr(res, f) for f, _ in ProbeResult._fields_}
+
+
+def ldmatrix_dump(num, trans, src_u16, row_elem):
+    """one warp's ldmatrix.x{num}[.trans] fragments: src (512,) 16-bit tensor on the GPU, row_elem
+    (32,) int32 element offsets; returns (32, num) int32 (register j of lane l)."""
+    _dev_check(src_u16, row_elem)
+    out = torch.empty((32, num), dtype=torch.int32, device=src_u16.device)
+    _check(lib().tcx_ldmatrix_dump(num, int(trans), _ptr(src_u16), _ptr(row_elem), _ptr(out), _stream(src_u16)))
+    return out

@@ -166,6 +166,15 @@ tcx_status tcx_mma_chain(tcx_dtype ab, int n_steps, int64_t count, const void* A
   return launch_chain(ab, n_steps, count, A0, Bs, Ds, (cudaStream_t)stream);
 }
 
+tcx_status tcx_ldmatrix_dump(int num, int trans, const void* src, const int32_t* row_elem, uint32_t* out,
+                             void* stream) {
+  if (!src || !row_elem || !out) return set_error(TCX_ERR_INVALID_VALUE, "tcx_ldmatrix_dump: NULL pointer");
+  DevInfo dev;
+  tcx_status st = current_device(&dev);
+  if (st != TCX_OK) return st;
+  return launch_ldmatrix_dump(num, trans, src, row_elem, out, (cudaStream_t)stream);
+}
+
 tcx_status tcx_mma_tiles_tc05(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, int64_t count, const void* A,
                               const void* B, const void* C, void* D, void* stream) {
   const bool fp = (ab == TCX_F16 || ab == TCX_BF16) && cd == TCX_F32 && m == 16 && n == 8 && k == 16;

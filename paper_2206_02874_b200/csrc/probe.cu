@@ -473,6 +473,9 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
     // throughput per SM: ILP MMAs of m x n x k per iteration, spread over cg SMs
     issuers_per_sm = 1.0 / cg;
     mnk = (double)m * n * k * ilp;
+  } else if (cfg->kind == TCX_PROBE_LDMATRIX || cfg->kind == TCX_PROBE_LDSHARED || cfg->kind == TCX_PROBE_TMEM_LD) {
+    st = run_probe_mem(dev, cfg, out);
+    goto done;
   } else {
     st = set_error(TCX_ERR_INVALID_VALUE, "tcx_probe: unknown kind %d", cfg->kind);
   }
