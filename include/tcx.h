@@ -115,14 +115,19 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
  *   with fewer are padded with the lowest free indices.  A group with >2 nonzeros is a
  *   violation: d_first_bad (device int64[2], written asynchronously) receives {row, group}
  *   of the first violation in row-major order, or {-1, -1}.  K % 32 == 0.
+ *   ab = TF32 (FP32 containers): the hardware's 1:2 rule (DESIGN.md R-C12) — every aligned pair
+ *   keeps its nonzero (or its lower element if both are zero); a pair with two nonzeros is a
+ *   violation, reported as its 4-group.  The canonical nibble then has i0 in {0,1}, i1 in {2,3}.
  * tcx_sp24_meta_hw_bytes / tcx_sp24_pack_meta: canonical -> the opaque hardware metadata
- *   image consumed by tcx_gemm_sp24 (tensor-memory interleaved layout).
- *   A nibble with i0 >= i1 is a violation reported through d_first_bad the same way.
- *   M % 128 == 0 and K % 128 == 0 for the packer (pad rows / K otherwise).
- * tcx_gemm_sp24: D = expand(A_vals, meta) x B + C.  ab = F16 or BF16, cd = F32.
- *   A_vals: M x K/2 (lda_vals >= K/2); meta_hw from tcx_sp24_pack_meta for the same M, K;
- *   B: N x K; C, D: M x N.  M % 128 == 0, K % 128 == 0, N % 16 == 0 required
- *   (else TCX_ERR_UNSUPPORTED).
+ *   image consumed by tcx_gemm_sp24 (tensor-memory layout per kind): M*K/8 bytes
+ *   (F16, BF16, S8) or M*K/4 (TF32).  A nibble with i0 >= i1 (TF32: not a 1:2 pattern) is a
+ *   violation reported through d_first_bad the same way.  M % 128 == 0 and K % 128 == 0
+ *   (TF32: K % 64 == 0) for the packer (pad rows / K otherwise).
+ * tcx_gemm_sp24: D = expand(A_vals, meta) x B + C.  (ab, cd) = (F16 | BF16 | TF32, F32) or
+ *   (S8, S32) with two's-complement wraparound.  meta_hw must come from tcx_sp24_pack_meta with
+ *   the same ab, M, K.  A_vals: M x K/2 (lda_vals >= K/2); B: N x K; C, D: M x N.
+ *   M % 128 == 0, N % 16 == 0 and K % 128 (F16/BF16), K % 256 (S8), K % 64 (TF32) == 0
+ *   required (else TCX_ERR_UNSUPPORTED).
  * ------------------------------------------------------------------------------------- */
 tcx_status tcx_sp24_compress(tcx_dtype ab, int64_t M, int64_t K, const void* A_dense, int64_t lda,
                              void* A_vals, uint32_t* meta_canon, int64_t* d_first_bad, void* stream);
