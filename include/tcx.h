@@ -93,7 +93,8 @@ typedef struct {
   int cta_group;   /* 1 or 2 (CTA pair, tcgen05 cta_group::2) */
   int max_ctas;    /* cap on persistent CTAs (0 = all SMs) */
   int group_m;     /* tile raster: cluster-tile rows that sweep N together (0 = default) */
-  int reserved[5];
+  int tile_n;      /* dense CTA-pair tile width: 256 or 512 (0 = library choice) */
+  int reserved[4];
 } tcx_gemm_opts;
 tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
                        const void* A, int64_t lda, const void* B, int64_t ldb,

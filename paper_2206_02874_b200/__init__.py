@@ -43,7 +43,7 @@ class TcxError(RuntimeError):
 
 class GemmOpts(ctypes.Structure):
     _fields_ = [("cta_group", ctypes.c_int), ("max_ctas", ctypes.c_int), ("group_m", ctypes.c_int),
-                ("reserved", ctypes.c_int * 5)]
+                ("tile_n", ctypes.c_int), ("reserved", ctypes.c_int * 4)]
 
 
 class ProbeConfig(ctypes.Structure):
@@ -169,7 +169,7 @@ def mma_chain(A0, Bs, tf32=False, Ds=None):
 
 
 # ---------------------------------------------------------------------------------------- GEMM
-def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0):
+def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, tile_n=0):
     """Dense D = A x B + C with A (M, K), B stored (N, K) ("row.col"), C/D (M, N)."""
     _dev_check(A, B, C, D)
     ab = ab_code(A, tf32)
@@ -178,7 +178,7 @@ def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0):
     cd = S32 if ab == S8 else F32
     if D is None:
         D = torch.empty((M, N), dtype=torch.int32 if cd == S32 else torch.float32, device=A.device)
-    opts = GemmOpts(cta_group, max_ctas, group_m)
+    opts = GemmOpts(cta_group, max_ctas, group_m, tile_n)
     _check(lib().tcx_gemm_ex(ab, cd, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
                              _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
                              ctypes.byref(opts), _stream(A)))

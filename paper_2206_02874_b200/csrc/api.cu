@@ -202,11 +202,14 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
   DevInfo dev;
   st = current_device(&dev);
   if (st != TCX_OK) return st;
-  GemmArgs g{ab, M, N, K, A, lda, B, ldb, C, ldc, D, ldd, nullptr, 2, 0, 0};
+  GemmArgs g{ab, M, N, K, A, lda, B, ldb, C, ldc, D, ldd, nullptr, 2, 0, 0, 0};
   if (opts) {
     if (opts->cta_group) g.cta_group = opts->cta_group;
     g.max_ctas = opts->max_ctas;
     g.group_m = opts->group_m;
+    if (opts->tile_n != 0 && opts->tile_n != 256 && opts->tile_n != 512)
+      return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: tile_n must be 0, 256 or 512");
+    g.tile_n = opts->tile_n;
   }
   if (K == 0) return launch_fill_c(g, (cudaStream_t)stream);
   return launch_gemm_dense(g, dev, (cudaStream_t)stream);
@@ -277,7 +280,7 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
   DevInfo dev;
   st = current_device(&dev);
   if (st != TCX_OK) return st;
-  GemmArgs g{ab, M, N, K, A_vals, lda_vals, B, ldb, C, ldc, D, ldd, meta_hw, 2, 0, 0};
+  GemmArgs g{ab, M, N, K, A_vals, lda_vals, B, ldb, C, ldc, D, ldd, meta_hw, 2, 0, 0, 0};
   if (opts) {
     if (opts->cta_group == 1 || opts->cta_group == 2) g.cta_group = opts->cta_group;
     g.max_ctas = opts->max_ctas;

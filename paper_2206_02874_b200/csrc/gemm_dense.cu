@@ -7,6 +7,11 @@
 //   warps 4..7  epilogue: tcgen05.ld 32x32b -> (+C) -> vectorised global stores
 // CG = 2 runs a CTA pair (cluster of 2, tcgen05 cta_group::2, UMMA M = 256): each CTA loads its
 // 128 rows of A and half (128 rows) of the N x K B tile; the leader issues the MMAs.
+// NH = 2 ("wide" tile, 256 x 512 per pair): every k-step issues two N = 256 MMAs that share the
+// A operand, so each stage moves 48 KiB per CTA for 2x the work of a 32 KiB NH = 1 stage — 25%
+// less L2->SM operand traffic per FLOP (the power-capped B200 turns that into clock); the two
+// halves fill all 512 TMEM columns, so the accumulator is single-buffered and the epilogue drains
+// half 0 first (its own empty barrier) so the next tile's half-0 MMAs can start early.
 // BK is one 128-byte swizzle row for every kind (64 f16/bf16, 32 tf32, 128 s8), and every
 // UMMA consumes 32 bytes of K (UMMA_K = 16 / 8 / 32).
 #include "tcx_internal.h"
@@ -23,15 +28,21 @@ constexpr int EPI_WARPS = 4;
 constexpr int NUM_THREADS = 256;
 constexpr int GROUP_M = 8;         // default raster: GROUP_M cluster-tile rows share B tiles in L2
 
-template <int CG>
+template <int CG, int NH>
 struct Cfg {
-  static constexpr int BN_LOAD = BN / CG;                        // B rows loaded per CTA
+  static constexpr int TILE_M = BM * CG;                         // output rows per tile
+  static constexpr int TILE_N = BN * NH;                         // output columns per tile
+  static constexpr int BN_LOAD = BN / CG;                        // B rows per CTA per N-half
+  static constexpr int HALF_BYTES = BN_LOAD * KBYTES;            // one N-half of B in smem
   static constexpr int A_BYTES = BM * KBYTES;                    // 16 KiB
-  static constexpr int B_BYTES = BN_LOAD * KBYTES;               // 32 or 16 KiB
+  static constexpr int B_BYTES = NH * HALF_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int STAGES = NH == 2 ? 4 : (CG == 1 ? 4 : 6);
+  static constexpr int NBUF = 2 / NH;                            // TMEM accumulator buffers
   static constexpr int SMEM_DATA = STAGES * STAGE_BYTES;
-  static constexpr int SMEM_TOTAL = SMEM_DATA + 1024 /*barriers*/ + 1024 /*align slack*/;
+  static constexpr int STG_BYTES = EPI_WARPS * 2 * 4096;         // epilogue: 2 x 4 KiB per warp
+  static constexpr int SMEM_TOTAL = SMEM_DATA + STG_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
+  static_assert(NH == 1 || CG == 2, "wide tiles need the CTA pair");
 };
 
 template <int KIND> struct KindT;
@@ -51,7 +62,8 @@ struct Smem {
   uint64_t full[8];
   uint64_t empty[8];
   uint64_t tmem_full[2];
-  uint64_t tmem_empty[2];
+  uint64_t tmem_empty[2];      // NH = 1: per buffer; NH = 2: per N-half of the single buffer
+  uint64_t cbar[EPI_WARPS][2]; // epilogue: C chunk landed in staging buffer b of warp e
   uint32_t tmem_base;
 };
 
@@ -67,22 +79,22 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64
   nt = r / gm;
 }
 
-template <int CG, int KIND>
+template <int CG, int KIND, int NH>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  int64_t M, int64_t N, int64_t K, const void* __restrict__ Cptr, int64_t ldc,
-                  void* __restrict__ Dptr, int64_t ldd, uint32_t idesc, int group_m) {
-  using C_ = Cfg<CG>;
+                  const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
+                  int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc, int group_m) {
+  using C_ = Cfg<CG, NH>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  Smem* sm = (Smem*)(smem + C_::SMEM_DATA);
+  Smem* sm = (Smem*)(smem + C_::SMEM_DATA + C_::STG_BYTES);
 
   const int warp = threadIdx.x / 32;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
 
-  const int64_t m_tiles = (M + BM * CG - 1) / (BM * CG);
-  const int64_t n_tiles = (N + BN - 1) / BN;
+  const int64_t m_tiles = (M + C_::TILE_M - 1) / C_::TILE_M;
+  const int64_t n_tiles = (N + C_::TILE_N - 1) / C_::TILE_N;
   const int64_t num_tiles = m_tiles * n_tiles;
   const int64_t k_blocks = (K * KindT<KIND>::ESIZE + KBYTES - 1) / KBYTES;
   const int64_t cluster_id = blockIdx.x / CG;
@@ -91,9 +103,10 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   if (threadIdx.x == 0) {
     for (int s = 0; s < C_::STAGES; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&sm->tmem_full[a], 1); mbar_init(&sm->tmem_empty[a], EPI_WARPS * CG); }
+    for (int w = 0; w < EPI_WARPS; ++w) { mbar_init(&sm->cbar[w][0], 1); mbar_init(&sm->cbar[w][1], 1); }
     fence_mbar_init();
   }
-  if (warp == 0 && elect_one()) { tma_prefetch(&tmA); tma_prefetch(&tmB); }
+  if (warp == 0 && elect_one()) { tma_prefetch(&tmA); tma_prefetch(&tmB); tma_prefetch(&tmC); tma_prefetch(&tmD); }
   if (warp == 2) { tmem_alloc<CG>(&sm->tmem_base, 512); tmem_relinquish<CG>(); }
   tc05_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
@@ -108,8 +121,8 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int64_t mt, nt;
         tile_coords(tile, m_tiles, n_tiles, group_m, mt, nt);
-        const int arow = (int)(mt * BM * CG + rank * BM);
-        const int brow = (int)(nt * BN + rank * C_::BN_LOAD);
+        const int arow = (int)(mt * C_::TILE_M + rank * BM);
+        const int brow = (int)(nt * C_::TILE_N + rank * C_::BN_LOAD);     // + h * BN for N-half h
         for (int64_t kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&sm->empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C_::STAGE_BYTES;
@@ -123,7 +136,8 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
             if (leader) mbar_arrive_expect_tx(&sm->full[stage], 2 * C_::STAGE_BYTES);
             const uint32_t bar = full0_cluster + stage * 8;
             tma_load_2d_cg2(sa, &tmA, bar, kx, arow);
-            tma_load_2d_cg2(sb, &tmB, bar, kx, brow);
+#pragma unroll
+            for (int h = 0; h < NH; ++h) tma_load_2d_cg2(sb + h * C_::HALF_BYTES, &tmB, bar, kx, brow + h * BN);
           }
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -134,101 +148,166 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     if (leader) {
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t acc_phase = 0;
+      auto issue = [&](int st, int h, int64_t kb, uint32_t tmem_d) {
+        const uint32_t sa = smem_u32(smem + st * C_::STAGE_BYTES);
+        const uint32_t sb = sa + C_::A_BYTES + h * C_::HALF_BYTES;              // N-half h's B rows
+#pragma unroll
+        for (int k = 0; k < KBYTES / UMMA_KBYTES; ++k)
+          umma<CG, KIND>(tmem_d + h * BN, sdesc(sa + k * UMMA_KBYTES, 16, 1024, 2),
+                         sdesc(sb + k * UMMA_KBYTES, 16, 1024, 2), idesc, (kb | k) ? 1u : 0u);
+      };
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        mbar_wait(&sm->tmem_empty[acc], acc_phase ^ 1);
-        tc05_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int64_t kb = 0; kb < k_blocks; ++kb) {
+        const uint32_t tmem_d = tmem_base + acc * BN * NH;
+        int64_t kb0 = 0;
+        if constexpr (NH == 1) {
+          mbar_wait(&sm->tmem_empty[acc], acc_phase ^ 1);
+          tc05_fence_after();
+        } else {
+          // single-buffered wide accumulator: the epilogue drains N-half 0 first, so issue half 0
+          // for the first L resident k-blocks before waiting for half 1 — the tensor pipe works
+          // while half 1 of the previous tile is still being read out.
+          const int64_t L = k_blocks < C_::STAGES ? k_blocks : C_::STAGES;
+          const int st0 = stage; const uint32_t ph0 = phase;
+          mbar_wait(&sm->tmem_empty[0], acc_phase ^ 1);
+          tc05_fence_after();
+          for (int64_t kb = 0; kb < L; ++kb) {
+            mbar_wait(&sm->full[stage], phase);
+            tc05_fence_after();
+            if (elect_one()) issue(stage, 0, kb, tmem_d);
+            __syncwarp();
+            if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
+          }
+          mbar_wait(&sm->tmem_empty[1], acc_phase ^ 1);
+          tc05_fence_after();
+          int st = st0; uint32_t ph = ph0;
+          for (int64_t kb = 0; kb < L; ++kb) {
+            if (elect_one()) {
+              issue(st, 1, kb, tmem_d);
+              tc05_commit<CG>(&sm->empty[st]);                   // both halves consumed the slot
+              if (kb == k_blocks - 1) tc05_commit<CG>(&sm->tmem_full[acc]);
+            }
+            __syncwarp();
+            if (++st == C_::STAGES) { st = 0; ph ^= 1; }
+          }
+          (void)ph;
+          kb0 = L;
+        }
+        for (int64_t kb = kb0; kb < k_blocks; ++kb) {
           mbar_wait(&sm->full[stage], phase);
           tc05_fence_after();
           if (elect_one()) {
-            const uint32_t sa = smem_u32(smem + stage * C_::STAGE_BYTES);
-            const uint32_t sb = sa + C_::A_BYTES;
 #pragma unroll
-            for (int k = 0; k < KBYTES / UMMA_KBYTES; ++k) {
-              const uint64_t ad = sdesc(sa + k * UMMA_KBYTES, 16, 1024, 2);
-              const uint64_t bd = sdesc(sb + k * UMMA_KBYTES, 16, 1024, 2);
-              umma<CG, KIND>(tmem_d, ad, bd, idesc, (kb | k) ? 1u : 0u);
-            }
+            for (int h = 0; h < NH; ++h) issue(stage, h, kb, tmem_d);
             tc05_commit<CG>(&sm->empty[stage]);                   // frees the smem slot
             if (kb == k_blocks - 1) tc05_commit<CG>(&sm->tmem_full[acc]);   // accumulator ready
           }
           __syncwarp();
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
         }
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (++acc == C_::NBUF) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else if (warp >= 4) {
     // ================= epilogue =================
+    // Per 32-column chunk: tcgen05.ld (thread = row) -> (+ C chunk, TMA-loaded into a 128B-swizzled
+    // 4 KiB staging buffer) -> result written back into that buffer -> one TMA store of the 32 x 32
+    // box (full-line, coalesced HBM writes; TMA clips rows >= M / columns >= N).  Two buffers per
+    // warp alternate; each tile's C is L2-prefetched one tile ahead, so the chunk loads hit L2.
     const int e = warp - 4;                       // TMEM lanes 32e .. 32e+31
     const int lane = threadIdx.x & 31;
-    int acc = 0; uint32_t acc_phase = 0;
+    constexpr int CH = NH * BN / 32;              // 32-column chunks per tile (over both halves)
+    uint8_t* stg = smem + C_::SMEM_DATA + e * 8192;
+    uint64_t* cbar = &sm->cbar[e][0];
+    uint32_t cph[2] = {0u, 0u};
     const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), 0) : smem_u32(&sm->tmem_empty[0]);
-    for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+    const int64_t my_tiles = cluster_id < num_tiles ? (num_tiles - 1 - cluster_id) / num_clusters + 1 : 0;
+    const int64_t nq = my_tiles * CH;
+    auto coords = [&](int64_t q, int& x, int& y) {
+      const int64_t it = q / CH;
       int64_t mt, nt;
-      tile_coords(tile, m_tiles, n_tiles, group_m, mt, nt);
-      const int64_t row = mt * BM * CG + rank * BM + e * 32 + lane;
-      const int64_t col0 = nt * BN;
+      tile_coords(cluster_id + it * num_clusters, m_tiles, n_tiles, group_m, mt, nt);
+      y = (int)(mt * C_::TILE_M + rank * BM + e * 32);
+      x = (int)(nt * C_::TILE_N + (q % CH) * 32);
+    };
+    auto prefetch_c_tile = [&](int64_t it) {
+      if (has_c && lane == 0 && it < my_tiles)
+        for (int ch = 0; ch < CH; ++ch) { int x, y; coords(it * CH + ch, x, y); tma_prefetch_2d(&tmC, x, y); }
+    };
+    auto load_c = [&](int64_t q) {
+      if (has_c && lane == 0 && q < nq) {
+        int x, y; coords(q, x, y);
+        mbar_arrive_expect_tx(&cbar[q & 1], 4096);
+        tma_load_2d(stg + (q & 1) * 4096, &tmC, &cbar[q & 1], x, y);
+      }
+    };
+    prefetch_c_tile(0);
+    load_c(0);
+    load_c(1);
+    int acc = 0; uint32_t acc_phase = 0;
+    const uint32_t lane_off = (uint32_t)(e * 32) << 16;
+    for (int64_t it = 0; it < my_tiles; ++it) {
+      prefetch_c_tile(it + 1);
       mbar_wait(&sm->tmem_full[acc], acc_phase);
       tc05_fence_after();
-      const bool row_ok = row < M;
+      uint32_t v[32], vn[32];
+      tmem_ld_32x32b_x32(tmem_base + acc * NH * BN + lane_off, vn);   // chunk 0
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        const int64_t c0 = col0 + ch * 32;
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem_base + acc * BN + ch * 32 + ((uint32_t)(e * 32) << 16), v);
-        uint32_t cv[32];
-        const bool full_chunk = c0 + 32 <= N;
-        if (Cptr != nullptr && row_ok && c0 < N) {
-          const uint32_t* crow = (const uint32_t*)Cptr + row * ldc + c0;
-          if (full_chunk) {
+      for (int ch = 0; ch < CH; ++ch) {
+        const int64_t q = it * CH + ch;
+        const int b = (int)(q & 1);
+        const int h = ch / (BN / 32);
+        tmem_ld_wait();                           // chunk ch has landed in vn
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              uint4 t = __ldg((const uint4*)(crow + j));
-              cv[j] = t.x; cv[j + 1] = t.y; cv[j + 2] = t.z; cv[j + 3] = t.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) cv[j] = (c0 + j < N) ? crow[j] : 0u;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) cv[j] = 0u;
+        for (int j = 0; j < 32; ++j) v[j] = vn[j];
+        if (ch + 1 < CH) {                        // read the next chunk while this one is stored
+          const int hn = (ch + 1) / (BN / 32);
+          tmem_ld_32x32b_x32(tmem_base + (acc * NH + hn) * BN + ((ch + 1) % (BN / 32)) * 32 + lane_off, vn);
         }
-        tmem_ld_wait();
-        if (ch == BN / 32 - 1) {
-          // accumulator fully read: hand the TMEM buffer back to the MMA warp
+        if (has_c) {
+          mbar_wait(&cbar[b], cph[b]);
+          cph[b] ^= 1u;
+        } else if (q >= 2) {
+          if (lane == 0) bulk_wait_read<1>();     // the store of chunk q-2 has read buffer b
+          __syncwarp();
+        }
+        if (ch % (BN / 32) == BN / 32 - 1 && (NH == 2 || ch == CH - 1)) {
+          // this part of the accumulator is read: hand it back to the MMA warp
+          // (NH = 1: the whole buffer `acc`; NH = 2: N-half h of the single buffer)
           tc05_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(tmem_empty_cluster + acc * 8);
+          if (lane == 0) mbar_arrive_cluster(tmem_empty_cluster + (NH == 2 ? h : acc) * 8);
         }
-        uint32_t out[32];
-        if constexpr (KIND == KIND_I8) {
+        uint8_t* rowp = stg + b * 4096 + lane * 128;          // this thread's row of the box
 #pragma unroll
-          for (int j = 0; j < 32; ++j) out[j] = v[j] + cv[j];          // wrap mod 2^32
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) out[j] = __float_as_uint(__fadd_rn(__uint_as_float(v[j]), __uint_as_float(cv[j])));
-          if (Cptr == nullptr) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) out[j] = v[j];                  // no C: D = acc exactly
+        for (int j = 0; j < 8; ++j) {
+          uint4* p = (uint4*)(rowp + ((j ^ (lane & 7)) * 16)); // SW128: chunk j at j ^ (row % 8)
+          uint4 o = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          if (has_c) {
+            const uint4 c = *p;
+            if constexpr (KIND == KIND_I8) {                   // S32: wrap mod 2^32
+              o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+            } else {                                          // FP32: one RNE add
+              o.x = __float_as_uint(__fadd_rn(__uint_as_float(o.x), __uint_as_float(c.x)));
+              o.y = __float_as_uint(__fadd_rn(__uint_as_float(o.y), __uint_as_float(c.y)));
+              o.z = __float_as_uint(__fadd_rn(__uint_as_float(o.z), __uint_as_float(c.z)));
+              o.w = __float_as_uint(__fadd_rn(__uint_as_float(o.w), __uint_as_float(c.w)));
+            }
           }
+          *p = o;
         }
-        if (row_ok && c0 < N) {
-          uint32_t* drow = (uint32_t*)Dptr + row * ldd + c0;
-          if (full_chunk) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *(uint4*)(drow + j) = make_uint4(out[j], out[j + 1], out[j + 2], out[j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) if (c0 + j < N) drow[j] = out[j];
-          }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          int x, y; coords(q, x, y);
+          tma_store_2d(&tmD, stg + b * 4096, x, y);
+          bulk_commit();
+          if (has_c && q + 2 < nq) bulk_wait_read<0>();      // buffer b is free again ...
         }
+        load_c(q + 2);                                        // ... for the C chunk two ahead
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == C_::NBUF) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) bulk_wait<0>();                            // stores complete before exit
   }
 
   tc05_fence_before();
@@ -245,9 +324,9 @@ __global__ void fill_c_kernel(const uint32_t* C, int64_t ldc, uint32_t* D, int64
   }
 }
 
-template <int CG, int KIND>
+template <int CG, int KIND, int NH>
 tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUtensorMapDataType dt, int a_fmt) {
-  using C_ = Cfg<CG>;
+  using C_ = Cfg<CG, NH>;
   constexpr int ES = KindT<KIND>::ESIZE;
   CUtensorMap tA, tB;
   tcx_status st = make_tmap_2d(&tA, dt, a.A, (uint64_t)a.K, (uint64_t)a.M, (uint64_t)(a.lda * ES),
@@ -256,10 +335,22 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
   st = make_tmap_2d(&tB, dt, a.B, (uint64_t)a.K, (uint64_t)a.N, (uint64_t)(a.ldb * ES),
                     KBYTES / ES, C_::BN_LOAD, CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != TCX_OK) return st;
-  auto kern = gemm_dense_kernel<CG, KIND>;
+  // C and D: 32 x 32 boxes of 4-byte elements (128-byte rows) through 128B-swizzled staging
+  CUtensorMap tC, tD;
+  st = make_tmap_2d(&tD, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.D, (uint64_t)a.N, (uint64_t)a.M, (uint64_t)(a.ldd * 4),
+                    32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (st != TCX_OK) return st;
+  if (a.C) {
+    st = make_tmap_2d(&tC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.C, (uint64_t)a.N, (uint64_t)a.M, (uint64_t)(a.ldc * 4),
+                      32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (st != TCX_OK) return st;
+  } else {
+    tC = tD;                                                  // unused (has_c = 0)
+  }
+  auto kern = gemm_dense_kernel<CG, KIND, NH>;
   TCX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_TOTAL));
-  const int64_t m_tiles = (a.M + BM * CG - 1) / (BM * CG);
-  const int64_t n_tiles = (a.N + BN - 1) / BN;
+  const int64_t m_tiles = (a.M + C_::TILE_M - 1) / C_::TILE_M;
+  const int64_t n_tiles = (a.N + C_::TILE_N - 1) / C_::TILE_N;
   int64_t clusters = m_tiles * n_tiles;
   int64_t max_clusters = dev.sm_count / CG;
   if (a.max_ctas > 0 && a.max_ctas / CG < max_clusters) max_clusters = a.max_ctas / CG > 0 ? a.max_ctas / CG : 1;
@@ -274,9 +365,8 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
   attr[0].val.clusterDim.x = CG; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr; cfg.numAttrs = 1;
   const uint32_t idesc = make_idesc(KIND, a_fmt, BM * CG, BN);
-  TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K, a.C,
-                                  (int64_t)a.ldc, a.D, (int64_t)a.ldd, idesc,
-                                  a.group_m > 0 ? a.group_m : GROUP_M));
+  TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
+                                  a.C ? 1 : 0, idesc, a.group_m > 0 ? a.group_m : GROUP_M));
   count_launch();
   return TCX_OK;
 }
@@ -293,21 +383,23 @@ tcx_status launch_fill_c(const GemmArgs& a, cudaStream_t s) {
   return TCX_OK;
 }
 
+template <int KIND>
+tcx_status launch_kind(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUtensorMapDataType dt, int a_fmt) {
+  if (a.cta_group == 1) return launch_t<1, KIND, 1>(a, dev, s, dt, a_fmt);
+  // 256 x 512 pair tiles only when asked: they cut L2->SM operand traffic by 25% (and run at a
+  // higher clock under the power cap), but the single-buffered accumulator exposes the epilogue,
+  // whose FP32 C read + D write bursts from all CTAs at once (profiles/r01_dense_tile_study.txt);
+  // the double-buffered 256 x 256 tile is faster for this API's FP32 C/D.
+  const bool wide = a.tile_n == 512;
+  return wide ? launch_t<2, KIND, 2>(a, dev, s, dt, a_fmt) : launch_t<2, KIND, 1>(a, dev, s, dt, a_fmt);
+}
+
 tcx_status launch_gemm_dense(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
-  const int cg = a.cta_group == 1 ? 1 : 2;
   switch (a.ab) {
-    case TCX_F16:
-      return cg == 1 ? launch_t<1, KIND_F16>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 0)
-                     : launch_t<2, KIND_F16>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 0);
-    case TCX_BF16:
-      return cg == 1 ? launch_t<1, KIND_F16>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 1)
-                     : launch_t<2, KIND_F16>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 1);
-    case TCX_TF32:
-      return cg == 1 ? launch_t<1, KIND_TF32>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2)
-                     : launch_t<2, KIND_TF32>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2);
-    case TCX_S8:
-      return cg == 1 ? launch_t<1, KIND_I8>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1)
-                     : launch_t<2, KIND_I8>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1);
+    case TCX_F16: return launch_kind<KIND_F16>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 0);
+    case TCX_BF16: return launch_kind<KIND_F16>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 1);
+    case TCX_TF32: return launch_kind<KIND_TF32>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2);
+    case TCX_S8: return launch_kind<KIND_I8>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1);
     default:
       return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm: unsupported ab type %d", (int)a.ab);
   }

@@ -45,7 +45,8 @@ struct SpCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + META_BYTES;
   static constexpr int STAGES = CG == 1 ? 2 : 4;
   static constexpr int SMEM_DATA = STAGES * STAGE_BYTES;
-  static constexpr int SMEM_TOTAL = SMEM_DATA + 1024 + 1024;
+  static constexpr int STG_BYTES = EPI_WARPS * 2 * 2048;   // epilogue: 2 x 2 KiB (32 rows x 16 cols) per warp
+  static constexpr int SMEM_TOTAL = SMEM_DATA + STG_BYTES + 1024 + 1024;
   static constexpr int META_COL = 512 - STAGES * META_COLS;    // metadata ring at the top of TMEM
   static constexpr int ACC_STRIDE = KIND == KIND_I8 ? BN : 256;   // second accumulator's column
   static_assert(B_HALF % 1024 == 0, "SW128 atoms need 1 KiB alignment");
@@ -57,6 +58,7 @@ struct Smem {
   uint64_t empty[8];
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
+  uint64_t cbar[EPI_WARPS][2]; // epilogue: C chunk landed in staging buffer b of warp e
   uint32_t tmem_base;
 };
 
@@ -74,14 +76,14 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64
 template <int CG, int KIND>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ CUtensorMap tmE, int64_t M, int64_t N, int64_t K,
-                 const uint32_t* __restrict__ Cptr, int64_t ldc, uint32_t* __restrict__ Dptr, int64_t ldd, uint32_t idesc,
+                 const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmC,
+                 const __grid_constant__ CUtensorMap tmD, int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc,
                  int group_m) {
   using C_ = SpCfg<CG, KIND>;
   constexpr int KL = C_::KL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  Smem* sm = (Smem*)(smem + C_::SMEM_DATA);
+  Smem* sm = (Smem*)(smem + C_::SMEM_DATA + C_::STG_BYTES);
 
   const int warp = threadIdx.x / 32;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -96,9 +98,10 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (threadIdx.x == 0) {
     for (int s = 0; s < C_::STAGES; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&sm->tmem_full[a], 1); mbar_init(&sm->tmem_empty[a], EPI_WARPS * CG); }
+    for (int w = 0; w < EPI_WARPS; ++w) { mbar_init(&sm->cbar[w][0], 1); mbar_init(&sm->cbar[w][1], 1); }
     fence_mbar_init();
   }
-  if (warp == 0 && elect_one()) { tma_prefetch(&tmA); tma_prefetch(&tmB); tma_prefetch(&tmE); }
+  if (warp == 0 && elect_one()) { tma_prefetch(&tmA); tma_prefetch(&tmB); tma_prefetch(&tmE); tma_prefetch(&tmC); tma_prefetch(&tmD); }
   if (warp == 2) { tmem_alloc<CG>(&sm->tmem_base, 512); tmem_relinquish<CG>(); }
   tc05_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
@@ -184,56 +187,98 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
     }
   } else if (warp >= 4) {
+    // per 16-column chunk: tcgen05.ld (thread = row) -> (+ C chunk TMA-loaded into a 64B-swizzled
+    // 2 KiB staging buffer) -> result back into the buffer -> one TMA store of the 32 x 16 box
+    // (coalesced full-line HBM writes, TMA clips rows >= M / columns >= N).  Two buffers per warp
+    // alternate; each tile's C is L2-prefetched one tile ahead (as in gemm_dense.cu).
     const int e = warp - 4;
     const int lane = threadIdx.x & 31;
-    int acc = 0; uint32_t acc_phase = 0;
+    constexpr int CH = BN / 16;
+    uint8_t* stg = smem + C_::SMEM_DATA + e * 4096;
+    uint64_t* cbar = &sm->cbar[e][0];
+    uint32_t cph[2] = {0u, 0u};
     const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), 0) : smem_u32(&sm->tmem_empty[0]);
-    for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+    const int64_t my_tiles = cluster_id < num_tiles ? (num_tiles - 1 - cluster_id) / num_clusters + 1 : 0;
+    const int64_t nq = my_tiles * CH;
+    auto coords = [&](int64_t q, int& x, int& y) {
       int64_t mt, nt;
-      tile_coords(tile, m_tiles, n_tiles, group_m, mt, nt);
-      const int64_t row = mt * BM * CG + rank * BM + e * 32 + lane;
-      const int64_t col0 = nt * BN;
+      tile_coords(cluster_id + (q / CH) * num_clusters, m_tiles, n_tiles, group_m, mt, nt);
+      y = (int)(mt * BM * CG + rank * BM + e * 32);
+      x = (int)(nt * BN + (q % CH) * 16);
+    };
+    auto prefetch_c_tile = [&](int64_t it) {
+      if (has_c && lane == 0 && it < my_tiles)
+        for (int ch = 0; ch < CH; ++ch) { int x, y; coords(it * CH + ch, x, y); tma_prefetch_2d(&tmC, x, y); }
+    };
+    auto load_c = [&](int64_t q) {
+      if (has_c && lane == 0 && q < nq) {
+        int x, y; coords(q, x, y);
+        mbar_arrive_expect_tx(&cbar[q & 1], 2048);
+        tma_load_2d(stg + (q & 1) * 2048, &tmC, &cbar[q & 1], x, y);
+      }
+    };
+    prefetch_c_tile(0);
+    load_c(0);
+    load_c(1);
+    int acc = 0; uint32_t acc_phase = 0;
+    const uint32_t lane_off = (uint32_t)(e * 32) << 16;
+    for (int64_t it = 0; it < my_tiles; ++it) {
+      prefetch_c_tile(it + 1);
       mbar_wait(&sm->tmem_full[acc], acc_phase);
       tc05_fence_after();
-      constexpr int NCH = BN / 16;
+      uint32_t v[16], vn[16];
+      tmem_ld_32x32b_x16(tmem_base + acc * C_::ACC_STRIDE + lane_off, vn);
 #pragma unroll 1
-      for (int ch = 0; ch < NCH; ++ch) {
-        const int64_t c0 = col0 + ch * 16;
-        uint32_t v[16];
-        tmem_ld_32x32b_x16(tmem_base + acc * C_::ACC_STRIDE + ch * 16 + ((uint32_t)(e * 32) << 16), v);
-        uint32_t cv[16];
-        const bool ok = c0 < N;          // N % 16 == 0: a chunk is all-in or all-out
-        if (Cptr != nullptr && ok) {
-          const uint4* crow = (const uint4*)(Cptr + row * ldc + c0);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint4 t = __ldg(crow + j);
-            cv[4 * j] = t.x; cv[4 * j + 1] = t.y; cv[4 * j + 2] = t.z; cv[4 * j + 3] = t.w;
-          }
-        }
+      for (int ch = 0; ch < CH; ++ch) {
+        const int64_t q = it * CH + ch;
+        const int b = (int)(q & 1);
         tmem_ld_wait();
-        if (ch == NCH - 1) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = vn[j];
+        if (ch + 1 < CH) tmem_ld_32x32b_x16(tmem_base + acc * C_::ACC_STRIDE + (ch + 1) * 16 + lane_off, vn);
+        if (ch == CH - 1) {
           tc05_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(tmem_empty_cluster + acc * 8);
         }
-        if (ok) {
-          uint4* drow = (uint4*)(Dptr + row * ldd + c0);
-          if (Cptr != nullptr) {
-            if constexpr (KIND == KIND_I8) {
+        if (has_c) {
+          mbar_wait(&cbar[b], cph[b]);
+          cph[b] ^= 1u;
+        } else if (q >= 2) {
+          if (lane == 0) bulk_wait_read<1>();     // the store of chunk q-2 has read buffer b
+          __syncwarp();
+        }
+        uint8_t* rowp = stg + b * 2048 + lane * 64;            // this thread's row of the box
 #pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = v[j] + cv[j];       // S32: wrap mod 2^32
-            } else {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__fadd_rn(__uint_as_float(v[j]), __uint_as_float(cv[j])));
+        for (int j = 0; j < 4; ++j) {
+          uint4* p = (uint4*)(rowp + ((j ^ ((lane >> 1) & 3)) * 16));   // SW64: chunk j at j ^ ((row/2) % 4)
+          uint4 o = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          if (has_c) {
+            const uint4 c = *p;
+            if constexpr (KIND == KIND_I8) {                   // S32: wrap mod 2^32
+              o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+            } else {                                          // FP32: one RNE add
+              o.x = __float_as_uint(__fadd_rn(__uint_as_float(o.x), __uint_as_float(c.x)));
+              o.y = __float_as_uint(__fadd_rn(__uint_as_float(o.y), __uint_as_float(c.y)));
+              o.z = __float_as_uint(__fadd_rn(__uint_as_float(o.z), __uint_as_float(c.z)));
+              o.w = __float_as_uint(__fadd_rn(__uint_as_float(o.w), __uint_as_float(c.w)));
             }
           }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) drow[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          *p = o;
         }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          int x, y; coords(q, x, y);
+          tma_store_2d(&tmD, stg + b * 2048, x, y);
+          bulk_commit();
+          if (has_c && q + 2 < nq) bulk_wait_read<0>();
+        }
+        load_c(q + 2);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) bulk_wait<0>();
   }
 
   tc05_fence_before();
@@ -259,6 +304,18 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   st = make_tmap_2d(&tE, CU_TENSOR_MAP_DATA_TYPE_UINT8, a.meta_hw, 128, meta_rows, 128, 128, 16 * C_::META_ATOMS,
                     CU_TENSOR_MAP_SWIZZLE_NONE);
   if (st != TCX_OK) return st;
+  // C and D: 32-row x 16-column boxes of 4-byte elements (64-byte rows), 64B-swizzled staging
+  CUtensorMap tC, tD;
+  st = make_tmap_2d(&tD, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.D, (uint64_t)a.N, (uint64_t)a.M, (uint64_t)(a.ldd * 4),
+                    16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (st != TCX_OK) return st;
+  if (a.C) {
+    st = make_tmap_2d(&tC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.C, (uint64_t)a.N, (uint64_t)a.M, (uint64_t)(a.ldc * 4),
+                      16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (st != TCX_OK) return st;
+  } else {
+    tC = tD;
+  }
   auto kern = gemm_sp24_kernel<CG, KIND>;
   TCX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_TOTAL));
   const int64_t tiles = (a.M / (BM * CG)) * ((a.N + BN - 1) / BN);
@@ -281,9 +338,8 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   const uint32_t cfmt = KIND == KIND_I8 ? 2u : 1u;
   const uint32_t idesc = (1u << 2) | (cfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
                          ((uint32_t)((BM * CG) >> 4) << 24);
-  TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tE, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
-                                  (const uint32_t*)a.C, (int64_t)a.ldc, (uint32_t*)a.D, (int64_t)a.ldd, idesc,
-                                  a.group_m > 0 ? a.group_m : GROUP_M));
+  TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tE, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
+                                  a.C ? 1 : 0, idesc, a.group_m > 0 ? a.group_m : GROUP_M));
   count_launch();
   return TCX_OK;
 }

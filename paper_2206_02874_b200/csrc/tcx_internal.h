@@ -52,6 +52,7 @@ struct GemmArgs {
   int cta_group;
   int max_ctas;
   int group_m;    // 0 = default
+  int tile_n;     // dense: 256 / 512 / 0 = auto
 };
 tcx_status launch_gemm_dense(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);
 tcx_status launch_gemm_sp24(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);

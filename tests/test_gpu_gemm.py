@@ -65,6 +65,38 @@ def test_gemm_integer_valued_bit_exact(fmt, cg):
     assert torch.equal(D.double(), ref)
 
 
+WIDE = [(256, 512, 128), (512, 1024, 256), (200, 600, 72), (264, 520, 40), (768, 1536, 1024), (256, 16, 64)]
+
+
+@pytest.mark.parametrize("tile_n", [512])
+@pytest.mark.parametrize("fmt", ["bf16", "tf32", "s8"])
+@pytest.mark.parametrize("shape", WIDE)
+def test_gemm_wide_tile_whole_matrix(fmt, shape, tile_n):
+    """the 256 x 512 pair tile (tile_n = 512; two N-halves share A), incl. ragged M/N/K and an N
+    smaller than one half."""
+    M, N, K = shape
+    if fmt == "s8":
+        K = max(16, (K + 15) // 16 * 16)
+    A, B, C = _problem(M, N, K, fmt, seed=M + 3 * N + K)
+    D = tcx.gemm(A, B, C, tf32=(fmt == "tf32"), tile_n=tile_n)
+    torch.cuda.synchronize()
+    _full_check(fmt, A, B, C, D)
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "s8"])
+def test_gemm_wide_equals_narrow_and_persistent(fmt):
+    """wide and narrow tiles run the same MMA sequence per output element: bit-identical D; and
+    the single-buffered wide accumulator survives many tiles per CTA pair (max_ctas = 2)."""
+    M, N, K = 1024, 2048, 768
+    A, B, C = _problem(M, N, K, fmt, seed=17)
+    Dn = tcx.gemm(A, B, C, tile_n=256)
+    Dw = tcx.gemm(A, B, C, tile_n=512)
+    Dp = tcx.gemm(A, B, C, tile_n=512, max_ctas=2)
+    torch.cuda.synchronize()
+    assert torch.equal(Dn.view(torch.int32), Dw.view(torch.int32))
+    assert torch.equal(Dw.view(torch.int32), Dp.view(torch.int32))
+
+
 @pytest.mark.parametrize("cg", [1, 2])
 def test_gemm_persistent_many_tiles_per_cta(cg):
     """few CTAs, many tiles each: exercises the smem ring and TMEM double-buffer phases."""

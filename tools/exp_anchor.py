@@ -33,7 +33,10 @@ def main():
         "cublas_bf16_out": lambda: torch.matmul(w.A, Bt, out=D16),
         "tcx_default": lambda: tcx.gemm(w.A, w.B, w.C, w.D),
         "tcx_noC": lambda: tcx.gemm(w.A, w.B, None, w.D),
-        "tcx_g16": lambda: tcx.gemm(w.A, w.B, w.C, w.D, group_m=16),
+        "tcx_narrow_noC": lambda: tcx.gemm(w.A, w.B, None, w.D, tile_n=256),
+        "tcx_narrow": lambda: tcx.gemm(w.A, w.B, w.C, w.D, tile_n=256),
+        "tcx_wide": lambda: tcx.gemm(w.A, w.B, w.C, w.D, tile_n=512),
+        "tcx_wide_g16": lambda: tcx.gemm(w.A, w.B, w.C, w.D, tile_n=512, group_m=16),
         "tcx_cg1": lambda: tcx.gemm(w.A, w.B, w.C, w.D, cta_group=1),
     }
     for rnd in range(2):
