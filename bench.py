@@ -50,7 +50,7 @@ def peaks():
 
 # nominal dense ratios vs bf16 (B200_PROFILING.md nominal table: tf32 1.1 vs 2.25; int8 = fp8 rate 4.5;
 # 2:4 sparse doubles the dense rate): peak for kind = measured bf16 peak x ratio
-KIND_RATIO = {"bf16": 1.0, "f16": 1.0, "tf32": 0.5, "s8": 2.0, "sp16": 2.0, "sp8": 4.0, "sptf32": 1.0}
+KIND_RATIO = {"bf16": 1.0, "f16": 1.0, "f16acc": 1.0, "tf32": 0.5, "s8": 2.0, "sp16": 2.0, "sp8": 4.0, "sptf32": 1.0}
 
 
 class ClockSampler:
@@ -140,6 +140,20 @@ class Work:
             self.tf32 = fmt == "tf32"
             self.kernel = "gemm_dense_kernel<2,%d>" % (0 if fmt == "bf16" else 1)
             self.step = lambda: tcx.gemm(self.A, self.B, self.C, self.D, tf32=self.tf32)
+            self.unit, self.bound = "TFLOP/s", "tensor"
+        elif cfg == "c3f16acc":              # NEXT-2: FP16 inputs, FP16 accumulator, FP16 C/D at C3's shape
+            M = N = K = 8192
+            self.kind = "f16acc"
+            self.shape = (M, N, K)
+            m0, m1 = self._rows(M)
+            self.A = g.normal_matrix((M, K), "f16", seed, g.STREAM_A, dev)[m0:m1].contiguous()
+            self.B = self._bcast(lambda: g.normal_matrix((N, K), "f16", seed, g.STREAM_B, dev))
+            self.C = torch.zeros(m1 - m0, N, dtype=torch.float16, device=dev)
+            self.D = torch.empty(m1 - m0, N, dtype=torch.float16, device=dev)
+            self.flops = 2.0 * (m1 - m0) * N * K
+            self.alg_bytes = 2 * (self.A.numel() + self.B.numel()) + 4 * (m1 - m0) * N
+            self.kernel = "gemm_dense_kernel<2,f16acc>"
+            self.step = lambda: tcx.gemm(self.A, self.B, self.C, self.D, f16_acc=True)
             self.unit, self.bound = "TFLOP/s", "tensor"
         elif cfg == "c4":
             M = N = K = 16384
@@ -273,7 +287,8 @@ class Work:
             ins = [self.A, self.B, self.C]
             out = self.D
             tf = getattr(self, "tf32", False)
-            self.e2e_op = lambda d: self.tcx.gemm(d[0], d[1], d[2], d[3], tf32=tf)
+            h = self.cfg == "c3f16acc"
+            self.e2e_op = lambda d: self.tcx.gemm(d[0], d[1], d[2], d[3], tf32=tf, f16_acc=h)
         self.h_ins = [t.cpu().pin_memory() for t in ins]
         self.hD = torch.empty_like(out, device="cpu").pin_memory()
         self.slots = [[torch.empty_like(t) for t in ins] + [torch.empty_like(out)] for _ in range(2)]
@@ -521,7 +536,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="tcx", choices=["tcx", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c3", "c3tf32", "c4", "c5", "c1", "c4sp", "c3sptf32"])
+    ap.add_argument("--config", default="c3", choices=["c3", "c3tf32", "c4", "c5", "c1", "c4sp", "c3sptf32", "c3f16acc"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -537,6 +552,7 @@ def main():
                  "c4": "INT8 GEMM M=N=K=16384 (configs[3])", "c5": "2:4 sparse FP16 GEMM M=65536 N=K=16384 (configs[4])",
                  "c1": "4096 m16n8k16 FP16 tiles (configs[0])",
                  "c4sp": "INT8 2:4 sparse GEMM M=N=K=16384 (NEXT-1 at configs[3]'s shape)",
+                 "c3f16acc": "FP16 GEMM with FP16 accumulator M=N=K=8192 (NEXT-2 at configs[2]'s shape)",
                  "c3sptf32": "TF32 1:2 sparse GEMM M=N=K=8192 (NEXT-1 at configs[2]'s shape)"}
     metric = "dense & 2:4-sparse MMA TFLOP/s (INT8 TOPS) per B200, % of tensor-core peak"
 
@@ -595,7 +611,7 @@ def main():
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None,
             "dtype": {"c3": "bf16", "c3tf32": "tf32", "c4": "s8", "c5": "f16", "c1": "f16", "c4sp": "s8",
-                      "c3sptf32": "tf32"}[args.config],
+                      "c3sptf32": "tf32", "c3f16acc": "f16"}[args.config],
             "data": "synthetic (seeded SplitMix64 / Box-Muller, tcxgen; generated on device)",
             "config": {"workload": cfg_names[args.config], "shape": list(work.shape),
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
@@ -608,7 +624,7 @@ def main():
                            "note": "cuBLAS via torch.matmul(A, B^T) on the same bf16 A, B, bf16 output (no C): "
                                    "context only, not part of the step"}
         also = {}
-        for extra in ("c3tf32", "c4", "c5", "c1", "c4sp", "c3sptf32"):
+        for extra in ("c3tf32", "c4", "c5", "c1", "c4sp", "c3sptf32", "c3f16acc"):
             try:
                 w2 = Work(extra, 0, 1, dev)
                 sampler.samples = []

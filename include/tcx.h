@@ -79,7 +79,10 @@ tcx_status tcx_mma_tiles(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, int64_
 
 /* ---------------------------------------------------------------------------------------
  * tcx_gemm — dense D = A x B + C, M x N x K, layouts above.
- * Supported: ab in {F16, BF16, TF32} with cd = F32;  ab = S8 with cd = S32.
+ * Supported: ab in {F16, BF16, TF32} with cd = F32;  ab = S8 with cd = S32;  ab = F16 with
+ * cd = F16 (FP16 accumulator, the f16.f16.f16.f16 MMA of PAPER.md:428-429 at GEMM scale: C and D
+ * are FP16, ldc*2 / ldd*2 multiples of 16 bytes, and C is the MMA's own C operand — loaded into
+ * the tensor-memory accumulator before the first MMA — not an epilogue add).
  * Any M, N >= 1 and K >= 1 subject to the alignment rules (ragged tiles are handled by
  * TMA out-of-bounds zero fill and predicated stores).  M == 0 or N == 0 is a no-op;
  * K == 0 gives D = C.

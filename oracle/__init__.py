@@ -62,6 +62,8 @@ def lib():
         L.tcxref_sum_round.argtypes = [i32, vp, vp, vp, i32, i32]; L.tcxref_sum_round.restype = u32
         L.tcxref_gemm_samples.argtypes = [i32, i64, vp, i64, vp, i64, vp, i64, i64, vp, vp, vp, vp, i32]
         L.tcxref_gemm_samples.restype = i32
+        L.tcxref_gemm_samples2.argtypes = [i32, i32, i64, vp, i64, vp, i64, vp, i64, i64, vp, vp, vp, vp, i32]
+        L.tcxref_gemm_samples2.restype = i32
         L.tcxref_sp24_expand.argtypes = [i32, i64, i64, vp, i64, vp, vp, i64]; L.tcxref_sp24_expand.restype = i64
         L.tcxref_sp24_compress.argtypes = [i32, i64, i64, vp, i64, vp, i64, vp]; L.tcxref_sp24_compress.restype = i64
         L.tcxref_sp12_compress.argtypes = [i64, i64, vp, i64, vp, i64, vp]; L.tcxref_sp12_compress.restype = i64
@@ -129,11 +131,12 @@ def sum_round(signs, mants, exps, out_fmt=F32, rz=False) -> int:
     return int(lib().tcxref_sum_round(len(s), _p(s), _p(m), _p(e), out_fmt, int(rz)))
 
 
-def gemm_samples(ab: int, A: np.ndarray, B: np.ndarray, C, rows, cols, nthreads: int | None = None):
+def gemm_samples(ab: int, A: np.ndarray, B: np.ndarray, C, rows, cols, nthreads: int | None = None, cd: int = F32):
     """D[rows[s], cols[s]] for A (M x K), B (N x K, 'col'), C (M x N or None).
 
-    Returns (out, abs) where out is uint32 bits (FP32 bits, or int32 bits for S8) and abs is
-    the float64 bound magnitude sum_k|a b| + |c| (FP only)."""
+    Returns (out, abs) where out is uint32 bits (FP32 bits, or int32 bits for S8; cd = F16: C is
+    FP16 and out holds RNE_fp16 bits of the exact value) and abs is the float64 bound magnitude
+    sum_k|a b| + |c| (FP only)."""
     A = np.ascontiguousarray(A); B = np.ascontiguousarray(B)
     assert A.dtype == _NP[ab] and B.dtype == _NP[ab], (A.dtype, B.dtype)
     M, K = A.shape
@@ -146,10 +149,10 @@ def gemm_samples(ab: int, A: np.ndarray, B: np.ndarray, C, rows, cols, nthreads:
     Cc = None
     if C is not None:
         Cc = np.ascontiguousarray(C)
-        assert Cc.shape == (M, N) and Cc.itemsize == 4
+        assert Cc.shape == (M, N) and Cc.itemsize == (2 if cd == F16 else 4)
     nt = nthreads or len(os.sched_getaffinity(0))
-    rc = lib().tcxref_gemm_samples(ab, K, _p(A), K, _p(B), K, _p(Cc) if Cc is not None else None,
-                                   N, n, _p(rows), _p(cols), _p(out), _p(absv), nt)
+    rc = lib().tcxref_gemm_samples2(ab, cd, K, _p(A), K, _p(B), K, _p(Cc) if Cc is not None else None,
+                                    N, n, _p(rows), _p(cols), _p(out), _p(absv), nt)
     assert rc == 0
     return out, absv
 

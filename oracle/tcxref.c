@@ -381,7 +381,7 @@ uint32_t tcxref_sum_round(int n, const int *signs, const uint64_t *mants, const 
 typedef struct {
   int ab; int64_t K; const void *A; int64_t lda; const void *B; int64_t ldb;
   const void *C; int64_t ldc; const int64_t *rows, *cols; uint32_t *out; double *abs_out;
-  int64_t s0, s1;
+  int64_t s0, s1; int cd;   /* cd: REF_F32 (FP32 C/D; INT32 for S8) or REF_F16 (FP16 C/D) */
 } job_t;
 
 static void *gemm_worker(void *arg) {
@@ -392,21 +392,22 @@ static void *gemm_worker(void *arg) {
     int64_t r = j->rows[s], c = j->cols[s];
     const char *a = (const char *)j->A + (size_t)(r * j->lda) * es;
     const char *b = (const char *)j->B + (size_t)(c * j->ldb) * es;
-    uint32_t cb = j->C ? ((const uint32_t *)j->C)[r * j->ldc + c] : 0u;
+    uint32_t cb = 0u;
+    if (j->C) cb = j->cd == REF_F16 ? ((const uint16_t *)j->C)[r * j->ldc + c] : ((const uint32_t *)j->C)[r * j->ldc + c];
     if (j->ab == REF_S8) {
       j->out[s] = (uint32_t)tcxref_dot_s8(j->K, (const int8_t *)a, (const int8_t *)b, (int32_t)cb);
     } else {
       double ab = 0.0;
-      j->out[s] = tcxref_dot_fp(j->ab, j->K, a, b, cb, &ab);
+      j->out[s] = tcxref_dot_fp2(j->ab, j->K, a, b, j->cd, cb, j->cd, 0, &ab);
       if (j->abs_out) j->abs_out[s] = ab;
     }
   }
   return NULL;
 }
 
-int tcxref_gemm_samples(int ab, int64_t K, const void *A, int64_t lda, const void *B, int64_t ldb,
-                        const void *C, int64_t ldc, int64_t nsamp, const int64_t *rows,
-                        const int64_t *cols, uint32_t *out, double *abs_out, int nthreads) {
+int tcxref_gemm_samples2(int ab, int cd, int64_t K, const void *A, int64_t lda, const void *B, int64_t ldb,
+                         const void *C, int64_t ldc, int64_t nsamp, const int64_t *rows,
+                         const int64_t *cols, uint32_t *out, double *abs_out, int nthreads) {
   pthread_t th[256];
   job_t jobs[256];
   int t;
@@ -415,13 +416,19 @@ int tcxref_gemm_samples(int ab, int64_t K, const void *A, int64_t lda, const voi
   for (t = 0; t < nthreads; t++) {
     job_t *j = &jobs[t];
     j->ab = ab; j->K = K; j->A = A; j->lda = lda; j->B = B; j->ldb = ldb; j->C = C; j->ldc = ldc;
-    j->rows = rows; j->cols = cols; j->out = out; j->abs_out = abs_out;
+    j->rows = rows; j->cols = cols; j->out = out; j->abs_out = abs_out; j->cd = cd == REF_F16 ? REF_F16 : REF_F32;
     j->s0 = nsamp * t / nthreads; j->s1 = nsamp * (t + 1) / nthreads;
     if (nthreads == 1) { gemm_worker(j); return 0; }
     if (pthread_create(&th[t], NULL, gemm_worker, j)) return -1;
   }
   for (t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
   return 0;
+}
+
+int tcxref_gemm_samples(int ab, int64_t K, const void *A, int64_t lda, const void *B, int64_t ldb,
+                        const void *C, int64_t ldc, int64_t nsamp, const int64_t *rows,
+                        const int64_t *cols, uint32_t *out, double *abs_out, int nthreads) {
+  return tcxref_gemm_samples2(ab, REF_F32, K, A, lda, B, ldb, C, ldc, nsamp, rows, cols, out, abs_out, nthreads);
 }
 
 /* ------------------------------------------------------------------------------------ */

@@ -23,7 +23,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtcx.so")
+# TCX_LIB_PATH selects another build of the same library (A/B experiments); never a fallback
+LIB_PATH = os.environ.get("TCX_LIB_PATH", os.path.join(_HERE, "libtcx.so"))
 
 F16, BF16, TF32, F32, S8, S32 = 0, 1, 2, 3, 4, 5
 _STATUS = {0: "TCX_OK", 1: "TCX_ERR_INVALID_VALUE", 2: "TCX_ERR_UNSUPPORTED", 3: "TCX_ERR_MISALIGNED",
@@ -169,15 +170,18 @@ def mma_chain(A0, Bs, tf32=False, Ds=None):
 
 
 # ---------------------------------------------------------------------------------------- GEMM
-def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, tile_n=0):
-    """Dense D = A x B + C with A (M, K), B stored (N, K) ("row.col"), C/D (M, N)."""
+def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, tile_n=0, f16_acc=False):
+    """Dense D = A x B + C with A (M, K), B stored (N, K) ("row.col"), C/D (M, N).
+    f16_acc: FP16 inputs with an FP16 accumulator (C, D float16; C is the MMA's C operand)."""
     _dev_check(A, B, C, D)
     ab = ab_code(A, tf32)
     M, K = A.shape
     N = B.shape[0]
-    cd = S32 if ab == S8 else F32
+    cd = S32 if ab == S8 else (F16 if f16_acc else F32)
+    if cd == F16 and C is not None and C.dtype != torch.float16:
+        raise ValueError("f16_acc: C must be float16")
     if D is None:
-        D = torch.empty((M, N), dtype=torch.int32 if cd == S32 else torch.float32, device=A.device)
+        D = torch.empty((M, N), dtype={S32: torch.int32, F16: torch.float16, F32: torch.float32}[cd], device=A.device)
     opts = GemmOpts(cta_group, max_ctas, group_m, tile_n)
     _check(lib().tcx_gemm_ex(ab, cd, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
                              _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),

@@ -99,12 +99,12 @@ static tcx_status check_gemm_common(const char* fn, tcx_dtype ab, tcx_dtype cd, 
     return set_error(TCX_ERR_INVALID_VALUE, "%s: leading dimension smaller than the row length", fn);
   if ((A && !aligned16(A)) || (B && !aligned16(B)) || (C && !aligned16(C)) || !aligned16(D))
     return set_error(TCX_ERR_MISALIGNED, "%s: device pointers must be 16-byte aligned", fn);
-  if ((lda * es) % 16 || (ldb * es) % 16 || (C && (ldc * 4) % 16) || (ldd * 4) % 16)
-    return set_error(TCX_ERR_MISALIGNED, "%s: lda*esize, ldb*esize, ldc*4, ldd*4 must be multiples of 16 bytes", fn);
+  const int cs = cd == TCX_F16 ? 2 : 4;
+  if ((lda * es) % 16 || (ldb * es) % 16 || (C && (ldc * cs) % 16) || (ldd * cs) % 16)
+    return set_error(TCX_ERR_MISALIGNED, "%s: lda*esize, ldb*esize, ldc*csize, ldd*csize must be multiples of 16 bytes", fn);
   if ((K * es) % 16) return set_error(TCX_ERR_MISALIGNED, "%s: K*esize must be a multiple of 16 bytes", fn);
   if (M > (1ll << 31) - 1 || N > (1ll << 31) - 1 || K > (1ll << 31) - 1)
     return set_error(TCX_ERR_UNSUPPORTED, "%s: dimension >= 2^31", fn);
-  (void)cd;
   return TCX_OK;
 }
 
@@ -193,7 +193,8 @@ tcx_status tcx_mma_tiles_tc05(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, i
 tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                        const void* B, int64_t ldb, const void* C, int64_t ldc, void* D, int64_t ldd,
                        const tcx_gemm_opts* opts, void* stream) {
-  const bool ok = ((ab == TCX_F16 || ab == TCX_BF16 || ab == TCX_TF32) && cd == TCX_F32) || (ab == TCX_S8 && cd == TCX_S32);
+  const bool ok = ((ab == TCX_F16 || ab == TCX_BF16 || ab == TCX_TF32) && cd == TCX_F32) || (ab == TCX_S8 && cd == TCX_S32) ||
+                  (ab == TCX_F16 && cd == TCX_F16);
   if (!ok) return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm: (ab=%d, cd=%d) not supported", ab, cd);
   tcx_status st = check_gemm_common("tcx_gemm", ab, cd, M, N, K, A, lda, B, ldb, C, ldc, D, ldd, K);
   if (st != TCX_OK || M == 0 || N == 0) return st;
@@ -202,7 +203,7 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
   DevInfo dev;
   st = current_device(&dev);
   if (st != TCX_OK) return st;
-  GemmArgs g{ab, M, N, K, A, lda, B, ldb, C, ldc, D, ldd, nullptr, 2, 0, 0, 0};
+  GemmArgs g{ab, cd, M, N, K, A, lda, B, ldb, C, ldc, D, ldd, nullptr, 2, 0, 0, 0};
   if (opts) {
     if (opts->cta_group) g.cta_group = opts->cta_group;
     g.max_ctas = opts->max_ctas;
@@ -280,7 +281,7 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
   DevInfo dev;
   st = current_device(&dev);
   if (st != TCX_OK) return st;
-  GemmArgs g{ab, M, N, K, A_vals, lda_vals, B, ldb, C, ldc, D, ldd, meta_hw, 2, 0, 0, 0};
+  GemmArgs g{ab, cd, M, N, K, A_vals, lda_vals, B, ldb, C, ldc, D, ldd, meta_hw, 2, 0, 0, 0};
   if (opts) {
     if (opts->cta_group == 1 || opts->cta_group == 2) g.cta_group = opts->cta_group;
     g.max_ctas = opts->max_ctas;

@@ -4,7 +4,7 @@
 //   warp 0      TMA producer: A (128 x BK) and B (BN_LOAD x BK) K-major tiles -> 128B-swizzled smem
 //   warp 1      MMA issuer (leader CTA only): tcgen05.mma kind::{f16,tf32,i8} into TMEM
 //   warp 2      TMEM allocator (512 columns = two 128 x 256 FP32/S32 accumulators)
-//   warps 4..7  epilogue: tcgen05.ld 32x32b -> (+C) -> vectorised global stores
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> (+C via TMA) -> swizzled smem -> TMA store
 // CG = 2 runs a CTA pair (cluster of 2, tcgen05 cta_group::2, UMMA M = 256): each CTA loads its
 // 128 rows of A and half (128 rows) of the N x K B tile; the leader issues the MMAs.
 // NH = 2 ("wide" tile, 256 x 512 per pair): every k-step issues two N = 256 MMAs that share the
@@ -45,16 +45,21 @@ struct Cfg {
   static_assert(NH == 1 || CG == 2, "wide tiles need the CTA pair");
 };
 
+// FP16 inputs with an FP16 accumulator (idesc c_format F16; the f16.f16.f16.f16 MMA of PAPER.md:428-429
+// at GEMM scale): C and D are FP16, and C is the MMA's own C operand — preloaded into the tensor-memory
+// accumulator by the epilogue warps (tcgen05.st) before the tile's first MMA (enable_input_d = 1).
+constexpr int KIND_F16ACC = 3;
 template <int KIND> struct KindT;
 template <> struct KindT<KIND_F16> { static constexpr int ESIZE = 2; };
+template <> struct KindT<KIND_F16ACC> { static constexpr int ESIZE = 2; };
 template <> struct KindT<KIND_TF32> { static constexpr int ESIZE = 4; };
 template <> struct KindT<KIND_I8> { static constexpr int ESIZE = 1; };
 
 // instruction descriptor (kind::f16 / tf32 / i8), K-major A and B, dense
 __host__ __device__ constexpr uint32_t make_idesc(int kind, int a_fmt, int M, int N) {
-  // c_format [4,6): F32 = 1, S32 = 2;  a_format [7,10), b_format [10,13);
+  // c_format [4,6): F16 = 0, F32 = 1, S32 = 2;  a_format [7,10), b_format [10,13);
   // N >> 3 at [17,23), M >> 4 at [24,29)
-  return ((kind == KIND_I8 ? 2u : 1u) << 4) | ((uint32_t)a_fmt << 7) | ((uint32_t)a_fmt << 10) |
+  return ((kind == KIND_I8 ? 2u : kind == KIND_F16ACC ? 0u : 1u) << 4) | ((uint32_t)a_fmt << 7) | ((uint32_t)a_fmt << 10) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
@@ -148,19 +153,24 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     if (leader) {
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t acc_phase = 0;
+      // FP16 accumulate with C: the accumulator holds C (preloaded) from the first MMA on
+      const bool acc16_c = KIND == KIND_F16ACC && has_c;
       auto issue = [&](int st, int h, int64_t kb, uint32_t tmem_d) {
         const uint32_t sa = smem_u32(smem + st * C_::STAGE_BYTES);
         const uint32_t sb = sa + C_::A_BYTES + h * C_::HALF_BYTES;              // N-half h's B rows
 #pragma unroll
         for (int k = 0; k < KBYTES / UMMA_KBYTES; ++k)
-          umma<CG, KIND>(tmem_d + h * BN, sdesc(sa + k * UMMA_KBYTES, 16, 1024, 2),
-                         sdesc(sb + k * UMMA_KBYTES, 16, 1024, 2), idesc, (kb | k) ? 1u : 0u);
+          umma<CG, KIND == KIND_F16ACC ? KIND_F16 : KIND>(tmem_d + h * BN, sdesc(sa + k * UMMA_KBYTES, 16, 1024, 2),
+                                                          sdesc(sb + k * UMMA_KBYTES, 16, 1024, 2), idesc,
+                                                          (acc16_c || (kb | k)) ? 1u : 0u);
       };
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         const uint32_t tmem_d = tmem_base + acc * BN * NH;
         int64_t kb0 = 0;
         if constexpr (NH == 1) {
-          mbar_wait(&sm->tmem_empty[acc], acc_phase ^ 1);
+          // FP16 accumulate: every use of a buffer (the first included) waits for the epilogue's
+          // arrival, which also means "C preloaded"
+          mbar_wait(&sm->tmem_empty[acc], KIND == KIND_F16ACC ? acc_phase : acc_phase ^ 1);
           tc05_fence_after();
         } else {
           // single-buffered wide accumulator: the epilogue drains N-half 0 first, so issue half 0
@@ -207,12 +217,106 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         if (++acc == C_::NBUF) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if (warp >= 4 && KIND == KIND_F16ACC) {
+    // ================= epilogue, FP16 accumulate =================
+    // D: tcgen05.ld (FP16 in the low half of each 32-bit column) -> packed f16x2 -> 64B-swizzled
+    // 2 KiB staging -> TMA store of the 32 x 32 FP16 box.  Then the drained buffer is refilled with
+    // the C of the tile that will use it next (two tiles ahead): TMA load of 32 x 32 FP16 boxes ->
+    // unpacked to one value per column -> tcgen05.st; the arrival on tmem_empty means "free + C".
+    const int e = warp - 4;
+    const int lane = threadIdx.x & 31;
+    constexpr int CH = BN / 32;
+    uint8_t* stg = smem + C_::SMEM_DATA + e * 8192;
+    uint64_t* cbar = &sm->cbar[e][0];
+    uint32_t cph[2] = {0u, 0u};
+    const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), 0) : smem_u32(&sm->tmem_empty[0]);
+    const int64_t my_tiles = cluster_id < num_tiles ? (num_tiles - 1 - cluster_id) / num_clusters + 1 : 0;
+    const uint32_t lane_off = (uint32_t)(e * 32) << 16;
+    auto coords = [&](int64_t it, int ch, int& x, int& y) {
+      int64_t mt, nt;
+      tile_coords(cluster_id + it * num_clusters, m_tiles, n_tiles, group_m, mt, nt);
+      y = (int)(mt * C_::TILE_M + rank * BM + e * 32);
+      x = (int)(nt * C_::TILE_N + ch * 32);
+    };
+    auto preload_c = [&](int64_t it, int buf) {
+      if (lane == 0) bulk_wait_read<0>();       // staging no longer read by earlier D stores
+      __syncwarp();
+      auto load = [&](int ch) {
+        if (lane == 0) {
+          int x, y; coords(it, ch, x, y);
+          mbar_arrive_expect_tx(&cbar[ch & 1], 2048);
+          tma_load_2d(stg + (ch & 1) * 2048, &tmC, &cbar[ch & 1], x, y);
+        }
+      };
+      load(0);
+      load(1);
+#pragma unroll 1
+      for (int ch = 0; ch < CH; ++ch) {
+        const int b = ch & 1;
+        mbar_wait(&cbar[b], cph[b]);
+        cph[b] ^= 1u;
+        const uint8_t* rowp = stg + b * 2048 + lane * 64;
+        uint32_t r[32];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint4 w = *(const uint4*)(rowp + ((j ^ ((lane >> 1) & 3)) * 16));   // SW64
+          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) { r[8 * j + 2 * i] = ws[i] & 0xFFFFu; r[8 * j + 2 * i + 1] = ws[i] >> 16; }
+        }
+        tmem_st_32x32b_x32(tmem_base + buf * BN + ch * 32 + lane_off, r);
+        __syncwarp();                             // every lane has read buffer b
+        if (ch + 2 < CH) load(ch + 2);
+      }
+      tmem_st_wait();
+    };
+    for (int t = 0; t < 2; ++t) {                 // buffers 0 and 1 start free (+ C of tiles 0, 1)
+      if (has_c && t < my_tiles) preload_c(t, t);
+      tc05_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tmem_empty_cluster + t * 8);
+    }
+    int acc = 0; uint32_t acc_phase = 0;
+    int64_t nstore = 0;
+    for (int64_t it = 0; it < my_tiles; ++it) {
+      mbar_wait(&sm->tmem_full[acc], acc_phase);
+      tc05_fence_after();
+#pragma unroll 1
+      for (int ch = 0; ch < CH; ++ch, ++nstore) {
+        const int b = (int)(nstore & 1);
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + acc * BN + ch * 32 + lane_off, v);
+        if (lane == 0 && nstore >= 2) bulk_wait_read<1>();   // store nstore-2 has read buffer b
+        __syncwarp();
+        tmem_ld_wait();
+        uint8_t* rowp = stg + b * 2048 + lane * 64;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint4 w = make_uint4((v[8 * j] & 0xFFFFu) | (v[8 * j + 1] << 16), (v[8 * j + 2] & 0xFFFFu) | (v[8 * j + 3] << 16),
+                                     (v[8 * j + 4] & 0xFFFFu) | (v[8 * j + 5] << 16), (v[8 * j + 6] & 0xFFFFu) | (v[8 * j + 7] << 16));
+          *(uint4*)(rowp + ((j ^ ((lane >> 1) & 3)) * 16)) = w;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          int x, y; coords(it, ch, x, y);
+          tma_store_2d(&tmD, stg + b * 2048, x, y);
+          bulk_commit();
+        }
+      }
+      if (has_c && it + 2 < my_tiles) { preload_c(it + 2, acc); nstore = 0; }
+      tc05_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tmem_empty_cluster + acc * 8);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) bulk_wait<0>();
   } else if (warp >= 4) {
     // ================= epilogue =================
     // Per 32-column chunk: tcgen05.ld (thread = row) -> (+ C chunk, TMA-loaded into a 128B-swizzled
     // 4 KiB staging buffer) -> result written back into that buffer -> one TMA store of the 32 x 32
     // box (full-line, coalesced HBM writes; TMA clips rows >= M / columns >= N).  Two buffers per
-    // warp alternate; each tile's C is L2-prefetched one tile ahead, so the chunk loads hit L2.
+    // warp alternate, the C chunk two ahead loading while this one is stored.
     const int e = warp - 4;                       // TMEM lanes 32e .. 32e+31
     const int lane = threadIdx.x & 31;
     constexpr int CH = NH * BN / 32;              // 32-column chunks per tile (over both halves)
@@ -229,10 +333,6 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       y = (int)(mt * C_::TILE_M + rank * BM + e * 32);
       x = (int)(nt * C_::TILE_N + (q % CH) * 32);
     };
-    auto prefetch_c_tile = [&](int64_t it) {
-      if (has_c && lane == 0 && it < my_tiles)
-        for (int ch = 0; ch < CH; ++ch) { int x, y; coords(it * CH + ch, x, y); tma_prefetch_2d(&tmC, x, y); }
-    };
     auto load_c = [&](int64_t q) {
       if (has_c && lane == 0 && q < nq) {
         int x, y; coords(q, x, y);
@@ -240,13 +340,11 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         tma_load_2d(stg + (q & 1) * 4096, &tmC, &cbar[q & 1], x, y);
       }
     };
-    prefetch_c_tile(0);
     load_c(0);
     load_c(1);
     int acc = 0; uint32_t acc_phase = 0;
     const uint32_t lane_off = (uint32_t)(e * 32) << 16;
     for (int64_t it = 0; it < my_tiles; ++it) {
-      prefetch_c_tile(it + 1);
       mbar_wait(&sm->tmem_full[acc], acc_phase);
       tc05_fence_after();
       uint32_t v[32], vn[32];
@@ -315,12 +413,13 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   if (warp == 2) { tc05_fence_after(); tmem_dealloc<CG>(tmem_base, 512); }
 }
 
-__global__ void fill_c_kernel(const uint32_t* C, int64_t ldc, uint32_t* D, int64_t ldd, int64_t M, int64_t N) {
+template <typename T>
+__global__ void fill_c_kernel(const T* C, int64_t ldc, T* D, int64_t ldd, int64_t M, int64_t N) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t total = M * N;
   for (; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = i / N, c = i % N;
-    D[r * ldd + c] = C ? C[r * ldc + c] : 0u;
+    D[r * ldd + c] = C ? C[r * ldc + c] : (T)0;
   }
 }
 
@@ -336,13 +435,16 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
                     KBYTES / ES, C_::BN_LOAD, CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != TCX_OK) return st;
   // C and D: 32 x 32 boxes of 4-byte elements (128-byte rows) through 128B-swizzled staging
+  // (FP16 accumulate: 32 x 32 boxes of FP16, 64-byte rows, 64B-swizzled)
+  constexpr bool H = KIND == KIND_F16ACC;
+  const CUtensorMapDataType cdt = H ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const CUtensorMapSwizzle csw = H ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+  const int ces = H ? 2 : 4;
   CUtensorMap tC, tD;
-  st = make_tmap_2d(&tD, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.D, (uint64_t)a.N, (uint64_t)a.M, (uint64_t)(a.ldd * 4),
-                    32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  st = make_tmap_2d(&tD, cdt, a.D, (uint64_t)a.N, (uint64_t)a.M, (uint64_t)(a.ldd * ces), 32, 32, csw);
   if (st != TCX_OK) return st;
   if (a.C) {
-    st = make_tmap_2d(&tC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.C, (uint64_t)a.N, (uint64_t)a.M, (uint64_t)(a.ldc * 4),
-                      32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    st = make_tmap_2d(&tC, cdt, a.C, (uint64_t)a.N, (uint64_t)a.M, (uint64_t)(a.ldc * ces), 32, 32, csw);
     if (st != TCX_OK) return st;
   } else {
     tC = tD;                                                  // unused (has_c = 0)
@@ -377,7 +479,10 @@ tcx_status launch_fill_c(const GemmArgs& a, cudaStream_t s) {
   int64_t total = a.M * a.N;
   int blocks = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
   if (blocks < 1) blocks = 1;
-  fill_c_kernel<<<blocks, 256, 0, s>>>((const uint32_t*)a.C, a.ldc, (uint32_t*)a.D, a.ldd, a.M, a.N);
+  if (a.cd == TCX_F16)
+    fill_c_kernel<uint16_t><<<blocks, 256, 0, s>>>((const uint16_t*)a.C, a.ldc, (uint16_t*)a.D, a.ldd, a.M, a.N);
+  else
+    fill_c_kernel<uint32_t><<<blocks, 256, 0, s>>>((const uint32_t*)a.C, a.ldc, (uint32_t*)a.D, a.ldd, a.M, a.N);
   TCX_CUDA_TRY(cudaGetLastError());
   count_launch();
   return TCX_OK;
@@ -395,6 +500,9 @@ tcx_status launch_kind(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CU
 }
 
 tcx_status launch_gemm_dense(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
+  if (a.cd == TCX_F16)     // FP16 accumulate (F16 inputs only; validated by the front end)
+    return a.cta_group == 1 ? launch_t<1, KIND_F16ACC, 1>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 0)
+                            : launch_t<2, KIND_F16ACC, 1>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 0);
   switch (a.ab) {
     case TCX_F16: return launch_kind<KIND_F16>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 0);
     case TCX_BF16: return launch_kind<KIND_F16>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 1);

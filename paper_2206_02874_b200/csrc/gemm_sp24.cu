@@ -190,7 +190,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     // per 16-column chunk: tcgen05.ld (thread = row) -> (+ C chunk TMA-loaded into a 64B-swizzled
     // 2 KiB staging buffer) -> result back into the buffer -> one TMA store of the 32 x 16 box
     // (coalesced full-line HBM writes, TMA clips rows >= M / columns >= N).  Two buffers per warp
-    // alternate; each tile's C is L2-prefetched one tile ahead (as in gemm_dense.cu).
+    // alternate, the C chunk two ahead loading while this one is stored (as in gemm_dense.cu).
     const int e = warp - 4;
     const int lane = threadIdx.x & 31;
     constexpr int CH = BN / 16;
@@ -206,10 +206,6 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       y = (int)(mt * BM * CG + rank * BM + e * 32);
       x = (int)(nt * BN + (q % CH) * 16);
     };
-    auto prefetch_c_tile = [&](int64_t it) {
-      if (has_c && lane == 0 && it < my_tiles)
-        for (int ch = 0; ch < CH; ++ch) { int x, y; coords(it * CH + ch, x, y); tma_prefetch_2d(&tmC, x, y); }
-    };
     auto load_c = [&](int64_t q) {
       if (has_c && lane == 0 && q < nq) {
         int x, y; coords(q, x, y);
@@ -217,13 +213,11 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         tma_load_2d(stg + (q & 1) * 2048, &tmC, &cbar[q & 1], x, y);
       }
     };
-    prefetch_c_tile(0);
     load_c(0);
     load_c(1);
     int acc = 0; uint32_t acc_phase = 0;
     const uint32_t lane_off = (uint32_t)(e * 32) << 16;
     for (int64_t it = 0; it < my_tiles; ++it) {
-      prefetch_c_tile(it + 1);
       mbar_wait(&sm->tmem_full[acc], acc_phase);
       tc05_fence_after();
       uint32_t v[16], vn[16];

@@ -43,6 +43,7 @@ tcx_status launch_chain(tcx_dtype ab, int n_steps, int64_t count, const void* A0
 
 struct GemmArgs {
   tcx_dtype ab;
+  tcx_dtype cd;
   int64_t M, N, K;
   const void* A; int64_t lda;
   const void* B; int64_t ldb;

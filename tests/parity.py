@@ -98,3 +98,24 @@ def fp16_bound_check(got_bits: np.ndarray, ref_bits: np.ndarray, absv: np.ndarra
         raise AssertionError(f"{what}: {int(bad.sum())} elements exceed the FP16 bar; first: got {got[i]!r} "
                              f"ref {ref[i]!r} bound {bound[i]!r}")
     return float((err / ulp).max()) if err.size else 0.0
+
+
+def fp16acc_gemm_bound_check(got_bits, ref_bits, absv, K, what=""):
+    """FP16-accumulate GEMM bar (DESIGN.md R-F16G): the accumulator itself is FP16 in tensor memory,
+    so every one of the ceil(K/16) instructions rounds its partial into FP16 (<= 1 ulp, 2^-10
+    relative, whatever the rounding mode; each partial is bounded by S = sum|ab| + |c|):
+        |D - D_ref| <= 2 * max(2^-10 |D_ref|, 2^-24) + (ceil(K/16) + 1) * 2^-10 * S."""
+    got = np.asarray(got_bits).astype(np.uint16).view(np.float16).astype(np.float64)
+    ref = np.asarray(ref_bits).astype(np.uint16).view(np.float16).astype(np.float64)
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isfinite(got), fin), f"{what}: finiteness differs"
+    got, ref, absv = got[fin], ref[fin], absv[fin]
+    bound = 2 * np.maximum(2.0 ** -10 * np.abs(ref), 2.0 ** -24) + (-(-K // 16) + 1) * 2.0 ** -10 * absv
+    err = np.abs(got - ref)
+    bad = err > bound
+    if bad.any():
+        i = int(np.argmax(bad))
+        raise AssertionError(f"{what}: {int(bad.sum())} beyond the FP16-accumulate bar; got {got[i]!r} ref {ref[i]!r} "
+                             f"bound {bound[i]!r}")
+    with np.errstate(divide="ignore", invalid="ignore"):
+        return float(np.nanmax(np.where(absv > 0, err / (2.0 ** -10 * absv), 0.0))) if err.size else 0.0

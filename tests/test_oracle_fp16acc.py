@@ -152,3 +152,18 @@ def test_model_fp16_acc_reduces_to_exact_and_rz(p):
                 assert out[i] & 0x7FFF == 0
             else:
                 assert out[i] == want, (i, rz, hex(out[i]), hex(want))
+
+
+def test_gemm_samples_fp16_cd_integer_exact():
+    """integer-valued FP16 GEMM with |sums| < 2048: the FP16 result is exact, so it must equal
+    numpy's exact float64 matmul cast to float16 (independent of the oracle's rounding code)."""
+    rng = np.random.default_rng(21)
+    M, N, K = 24, 20, 64
+    A = rng.integers(-3, 4, (M, K)).astype(np.float16)
+    B = rng.integers(-3, 4, (N, K)).astype(np.float16)
+    C = rng.integers(-500, 500, (M, N)).astype(np.float16)
+    ii, jj = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+    out, _ = O.gemm_samples(O.F16, A.view(np.uint16), B.view(np.uint16), C.view(np.uint16), ii.ravel(), jj.ravel(),
+                            cd=O.F16)
+    ref = (A.astype(np.float64) @ B.astype(np.float64).T + C.astype(np.float64)).astype(np.float16)
+    assert np.array_equal(out.astype(np.uint16).reshape(M, N), ref.view(np.uint16))
