@@ -172,18 +172,22 @@ tcx_status tcx_round_tf32(const float* in, float* out, int64_t n, void* stream);
  *                          (lane l reads byte l*4*n; Table ldshared-latency)
  *   TCX_PROBE_TMEM_LD      tcgen05.ld.sync.aligned.32x32b.x{m} + tcgen05.wait::ld, m in
  *                          {1,2,4,8,16,32}: B200's accumulator read-out (warps <= 16)
+ *   TCX_PROBE_TMA_LOAD     ilp cp.async.bulk.tensor.2d loads of an m-row x n-byte box (L2-resident
+ *                          16 MiB source) per mbarrier wait, one thread per CTA: operand staging
+ *   TCX_PROBE_TC05_CP      ilp tcgen05.cp.cta_group::1.128x128b (2 KiB smem -> TMEM) per commit
  * Synchronous; allocates and frees its own scratch.  Shapes not implemented ->
  * TCX_ERR_UNSUPPORTED.
  * ------------------------------------------------------------------------------------- */
 typedef enum { TCX_PROBE_MMA_SYNC = 0, TCX_PROBE_MMA_SP_SYNC = 1, TCX_PROBE_TC05 = 2,
                TCX_PROBE_TC05_SP = 3, TCX_PROBE_LDMATRIX = 4, TCX_PROBE_LDSHARED = 5,
-               TCX_PROBE_TMEM_LD = 6 } tcx_probe_kind;
+               TCX_PROBE_TMEM_LD = 6, TCX_PROBE_TMA_LOAD = 7, TCX_PROBE_TC05_CP = 8 } tcx_probe_kind;
 typedef struct {
   int kind;          /* tcx_probe_kind */
   int ab, cd;        /* tcx_dtype */
   int m, n, k;       /* instruction shape (k = logical k for sparse) */
   int cta_group;     /* tcgen05 only: 1 or 2 */
-  int warps;         /* mma.sync: warps per CTA; tcgen05: unused (1 issuer per CTA) */
+  int warps;         /* mma.sync / data movement: warps per CTA; tcgen05: cap on the distinct
+                        accumulators the ILP MMAs rotate over (0 = as many as TMEM holds) */
   int ilp;           /* independent MMAs per iteration */
   int iters;         /* timed iterations */
   int repeats;       /* repeated launches; min and median reported */

@@ -444,7 +444,8 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
                            ((uint32_t)(m >> 4) << 24);
     const int acc_cols = n;
     const int max_acc = (sp ? 448 : 512) / acc_cols;
-    const int n_acc = std::max(1, std::min(ilp, max_acc));
+    // independent accumulators the ILP MMAs rotate over (cfg->warps > 0 caps it; 1 = one chain)
+    const int n_acc = std::max(1, std::min(cfg->warps > 0 ? std::min(ilp, cfg->warps) : ilp, max_acc));
     const int clusters = std::max(1, nsm / cg);
     issuers_per_sm = 1.0 / cg;           // one MMA stream per CTA pair covers 2 SMs
     mnk = (double)m * n * k;
@@ -473,7 +474,8 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
     // throughput per SM: ILP MMAs of m x n x k per iteration, spread over cg SMs
     issuers_per_sm = 1.0 / cg;
     mnk = (double)m * n * k * ilp;
-  } else if (cfg->kind == TCX_PROBE_LDMATRIX || cfg->kind == TCX_PROBE_LDSHARED || cfg->kind == TCX_PROBE_TMEM_LD) {
+  } else if (cfg->kind == TCX_PROBE_LDMATRIX || cfg->kind == TCX_PROBE_LDSHARED || cfg->kind == TCX_PROBE_TMEM_LD ||
+             cfg->kind == TCX_PROBE_TMA_LOAD || cfg->kind == TCX_PROBE_TC05_CP) {
     st = run_probe_mem(dev, cfg, out);
     goto done;
   } else {

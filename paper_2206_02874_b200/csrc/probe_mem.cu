@@ -10,6 +10,9 @@
 //   TMEM_LD   B200's staging path out of the tensor core: tcgen05.ld.sync.aligned.32x32b.x{N}
 //             (+ tcgen05.wait::ld), 32 lanes x N x 4 bytes per warp — the epilogue's read of the
 //             accumulator (not in the paper: B200-specific)
+//   TMA_LOAD  the GEMMs' operand staging: ILP cp.async.bulk.tensor.2d boxes (m rows x n bytes) in
+//             flight per mbarrier wait, from an L2-resident 16 MiB buffer
+//   TC05_CP   the sparse path's metadata staging: ILP tcgen05.cp.128x128b (2 KiB) per commit
 // Throughput is bytes/clk/SM.  Also: tcx_ldmatrix_dump, the functional check
 // that ldmatrix delivers exactly the fragments its definition names.
 #include <algorithm>
@@ -177,6 +180,76 @@ __global__ void __launch_bounds__(512, 1) probe_tmem_ld_kernel(int iters, int il
   if (warp == 0) { tc05_fence_after(); tmem_dealloc<1>(tbase_s, 512); }
 }
 
+// ---------------------------------------------------------------- TMA 2D loads (global -> smem)
+// B200's operand staging: one thread issues ILP cp.async.bulk.tensor.2d loads of a
+// (box_rows x box_bytes) box into distinct smem slots, then waits on the mbarrier (the iteration's
+// sync).  The source is a 16 MiB buffer (L2-resident after the warm-up): L2-hit latency/bandwidth.
+__global__ void __launch_bounds__(32, 1) probe_tma_kernel(const __grid_constant__ CUtensorMap tm, int iters, int ilp,
+                                                          int box_rows, uint32_t box_bytes, int rows_total,
+                                                          long long* cycles, long long* ns) {
+  extern __shared__ uint8_t dyn[];
+  uint8_t* buf = (uint8_t*)(((uintptr_t)dyn + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  __syncwarp();
+  if (threadIdx.x != 0) return;
+  uint32_t phase = 0;
+  long long t0 = 0; uint64_t g0 = 0;
+  int y = (blockIdx.x * 97) % (rows_total - box_rows);
+  for (int it = -4; it < iters; ++it) {
+    if (it == 0) { t0 = clock64(); g0 = gtimer(); }
+    mbar_arrive_expect_tx(&bar, (uint32_t)ilp * box_bytes);
+    for (int s = 0; s < ilp; ++s) {
+      tma_load_2d(buf + s * box_bytes, &tm, &bar, 0, y);
+      y += box_rows;
+      if (y + box_rows > rows_total) y = 0;
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+  }
+  const long long t1 = clock64();
+  const uint64_t g1 = gtimer();
+  cycles[blockIdx.x * 32] = t1 - t0;
+  ns[blockIdx.x * 32] = (long long)(g1 - g0);
+}
+
+// ---------------------------------------------------------------- tcgen05.cp (smem -> TMEM)
+// the sparse path's metadata staging: ILP tcgen05.cp.cta_group::1.128x128b (2 KiB each) into
+// distinct TMEM columns, then tcgen05.commit -> mbarrier wait.
+__global__ void __launch_bounds__(128, 1) probe_tc05_cp_kernel(int iters, int ilp, long long* cycles, long long* ns) {
+  __shared__ __align__(1024) uint8_t src[16 * 2048];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tb;
+  const int warp = threadIdx.x / 32;
+  for (int i = threadIdx.x; i < 16 * 2048 / 16; i += blockDim.x) ((uint4*)src)[i] = make_uint4(i, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  if (warp == 0) { tmem_alloc<1>(&tb, 512); tmem_relinquish<1>(); }
+  tc05_fence_before();
+  __syncthreads();
+  tc05_fence_after();
+  if (threadIdx.x == 0) {
+    uint32_t phase = 0;
+    long long t0 = 0; uint64_t g0 = 0;
+    for (int it = -4; it < iters; ++it) {
+      if (it == 0) { t0 = clock64(); g0 = gtimer(); }
+      for (int s = 0; s < ilp; ++s)
+        tc05_cp_128x128b<1>(tb + (uint32_t)((s * 4) & 511), sdesc(smem_u32(src) + (s & 15) * 2048, 128, 128, 0));
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_u32(&bar)) : "memory");
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      tc05_fence_after();
+    }
+    const long long t1 = clock64();
+    const uint64_t g1 = gtimer();
+    cycles[blockIdx.x * 32] = t1 - t0;
+    ns[blockIdx.x * 32] = (long long)(g1 - g0);
+  }
+  tc05_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc05_fence_after(); tmem_dealloc<1>(tb, 512); }
+}
+
 // ---------------------------------------------------------------- functional ldmatrix dump
 // src: 512 b16 elements (4 matrices x 8 rows x 16 B, row-major), row_elem[l] = element offset of
 // the row lane l addresses; out[l * N + j] = register j of lane l.
@@ -226,6 +299,8 @@ tcx_status run_probe_mem(const DevInfo& dev, const tcx_probe_config* cfg, tcx_pr
   TCX_CUDA_TRY(cudaMalloc(&d_sink, 16));
   tcx_status st = TCX_OK;
   double bytes_per_warp_iter = 0;
+  int warps_eff = warps;              // timing slots per CTA (1 for the single-thread TMA / cp probes)
+  void* tma_src = nullptr;
   std::vector<double> per_iter, per_ns;
   for (int rep = 0; rep < reps && st == TCX_OK; ++rep) {
     cudaError_t le = cudaSuccess;
@@ -264,6 +339,30 @@ tcx_status run_probe_mem(const DevInfo& dev, const tcx_probe_config* cfg, tcx_pr
       else if (n == 16) T(16); else if (n == 32) T(32);
       else { st = set_error(TCX_ERR_UNSUPPORTED, "tcx_probe: tcgen05.ld 32x32b.x{1,2,4,8,16,32}"); break; }
 #undef T
+    } else if (cfg->kind == TCX_PROBE_TMA_LOAD) {
+      // box = m rows x n bytes (n in {16..256}, multiple of 16), u8 tensor of 4096 rows x 4096 B
+      const int rows = cfg->m > 0 ? cfg->m : 128, inner = cfg->n > 0 ? cfg->n : 128;
+      if (rows > 256 || inner > 256 || inner % 16 || rows * inner * ilp > 200 * 1024) {
+        st = set_error(TCX_ERR_UNSUPPORTED, "tcx_probe: TMA box m <= 256 rows, n <= 256 bytes (x16), ilp*box <= 200 KiB");
+        break;
+      }
+      if (!tma_src) {
+        if (cudaMalloc(&tma_src, 4096u * 4096u) != cudaSuccess) { st = set_error(TCX_ERR_CUDA, "probe: cudaMalloc"); break; }
+        cudaMemset(tma_src, 1, 4096u * 4096u);
+      }
+      CUtensorMap tm;
+      st = make_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, tma_src, 4096, 4096, 4096, (uint32_t)inner, (uint32_t)rows,
+                        CU_TENSOR_MAP_SWIZZLE_NONE);
+      if (st != TCX_OK) break;
+      const int smem = rows * inner * ilp + 1024;
+      cudaFuncSetAttribute(probe_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      bytes_per_warp_iter = (double)rows * inner * ilp;
+      probe_tma_kernel<<<nsm, 32, smem>>>(tm, iters, ilp, rows, (uint32_t)(rows * inner), 4096, d_cyc, d_ns);
+      warps_eff = 1;
+    } else if (cfg->kind == TCX_PROBE_TC05_CP) {
+      bytes_per_warp_iter = 2048.0 * ilp;
+      probe_tc05_cp_kernel<<<nsm, 128>>>(iters, ilp, d_cyc, d_ns);
+      warps_eff = 1;
     } else {
       st = set_error(TCX_ERR_INVALID_VALUE, "tcx_probe: unknown kind %d", cfg->kind);
       break;
@@ -277,7 +376,7 @@ tcx_status run_probe_mem(const DevInfo& dev, const tcx_probe_config* cfg, tcx_pr
     cudaMemcpy(nsv.data(), d_ns, nsv.size() * sizeof(long long), cudaMemcpyDeviceToHost);
     std::vector<double> c2, n2;
     for (int b = 0; b < nsm; ++b)
-      for (int w = 0; w < warps; ++w) { c2.push_back((double)cyc[b * 32 + w]); n2.push_back((double)nsv[b * 32 + w]); }
+      for (int w = 0; w < warps_eff; ++w) { c2.push_back((double)cyc[b * 32 + w]); n2.push_back((double)nsv[b * 32 + w]); }
     per_iter.push_back(*std::max_element(c2.begin(), c2.end()) / iters);   // the slowest warp bounds the SM
     per_ns.push_back(*std::max_element(n2.begin(), n2.end()) / iters);
   }
@@ -289,7 +388,7 @@ tcx_status run_probe_mem(const DevInfo& dev, const tcx_probe_config* cfg, tcx_pr
     const double nsi = med(per_ns);
     out->ns_per_iter = nsi;
     out->sm_mhz = nsi > 0 ? m / nsi * 1000.0 : 0;
-    out->fma_per_clk_per_sm = warps * bytes_per_warp_iter / m;          // bytes/clk/SM
+    out->fma_per_clk_per_sm = warps_eff * bytes_per_warp_iter / m;      // bytes/clk/SM
     out->iters = iters;
     uint32_t sink = 0;
     cudaMemcpy(&sink, d_sink, 4, cudaMemcpyDeviceToHost);
@@ -298,6 +397,7 @@ tcx_status run_probe_mem(const DevInfo& dev, const tcx_probe_config* cfg, tcx_pr
   cudaFree(d_cyc);
   cudaFree(d_ns);
   cudaFree(d_sink);
+  if (tma_src) cudaFree(tma_src);
   return st;
 }
 

@@ -11,7 +11,7 @@
 namespace tcx {
 namespace {
 
-constexpr int WARPS = 8;
+constexpr int WARPS = 8;             // warps per CTA (4..32 measured equal: profiles/r01_tiles_launch_sweep.jsonl)
 
 template <int AB>  // 0 f16, 1 bf16
 __device__ __forceinline__ void mma_16816(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(WARPS * 32) tiles_s8_kernel(const int8_t* __re
 int grid_for(int64_t count) {
   int64_t warps = count;
   int64_t blocks = (warps + WARPS - 1) / WARPS;
-  const int64_t cap = 148 * 16;   // persistent-ish: 16 CTAs of 8 warps per SM at most
+  const int64_t cap = 148 * (128 / WARPS);   // persistent-ish: 2 x the 64 resident warps per SM
   return (int)(blocks < cap ? blocks : cap);
 }
 

@@ -61,6 +61,17 @@ def test_tmem_ld_runs_and_scales():
     assert a["latency_cycles"] > 0 and b["fma_per_clk_per_sm"] >= a["fma_per_clk_per_sm"]
 
 
+def test_tma_and_tc05_cp_probes():
+    """B200's staging path (SURVEY §8(f) NEXT-3): TMA 2D box loads from L2 and tcgen05.cp smem->TMEM;
+    more boxes in flight per wait raise bytes/clk/SM (latency is amortised)."""
+    t1 = _p("tma_load", m=128, n=128, ilp=1, num_sms=148)
+    t8 = _p("tma_load", m=128, n=128, ilp=8, num_sms=148)
+    assert t1["latency_cycles"] > 100 and t8["fma_per_clk_per_sm"] > 2 * t1["fma_per_clk_per_sm"]
+    c1 = _p("tc05_cp", ilp=1)
+    c8 = _p("tc05_cp", ilp=8)
+    assert c1["latency_cycles"] > 0 and c8["fma_per_clk_per_sm"] > c1["fma_per_clk_per_sm"]
+
+
 def test_data_movement_sweep_report():
     rep = {"units": {"latency": "cycles per iteration (clock64)", "throughput": "bytes/clk/SM"},
            "paper_A100_context": {
@@ -89,6 +100,18 @@ def test_data_movement_sweep_report():
                 r = _p("tmem_ld", m=n, warps=w, ilp=ilp, repeats=2)
                 rows[f"({w},{ilp})"] = [round(r["latency_cycles"], 2), round(r["fma_per_clk_per_sm"], 2)]
         rep["tmem_ld"][f"32x32b.x{n}"] = rows
+    rep["tma_load"] = {}
+    for rows, inner in ((128, 128), (256, 128), (64, 128), (128, 256)):
+        row = {}
+        for ilp in (1, 2, 4, 8):
+            if rows * inner * ilp > 200 * 1024:
+                continue
+            for nsm in (1, 148):
+                r = _p("tma_load", m=rows, n=inner, ilp=ilp, num_sms=nsm, repeats=2)
+                row[f"ilp{ilp}_sms{nsm}"] = [round(r["latency_cycles"], 1), round(r["fma_per_clk_per_sm"], 2)]
+        rep["tma_load"][f"box{rows}x{inner}B"] = row
+    rep["tc05_cp_128x128b"] = {f"ilp{ilp}": [round(r["latency_cycles"], 1), round(r["fma_per_clk_per_sm"], 2)]
+                                for ilp in (1, 2, 4, 8) for r in [_p("tc05_cp", ilp=ilp, repeats=2)]}
     out = os.environ.get("TCX_REPORT_DIR", "gpurun_out")
     os.makedirs(out, exist_ok=True)
     with open(os.path.join(out, "data_movement_report.json"), "w") as f:
