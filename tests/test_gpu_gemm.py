@@ -186,3 +186,22 @@ def test_config4_full_size_int8_bit_exact():
         lhs = (Dd @ r).long()
         rhs = (Ad @ (Bd.T @ r) + Cd @ r).long()   # D = A B^T (B stored N x K)
         assert torch.equal((lhs - rhs) & 0xFFFFFFFF, torch.zeros_like(lhs))
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "s8"])
+def test_gemm_in_place_d_aliases_c(fmt):
+    """D may alias C (include/tcx.h): every C chunk is read before the D chunk at the same place is
+    written (TMA-store epilogue), so in-place equals out-of-place bit for bit."""
+    M, N, K = 512, 768, 256
+    A, B, C = _problem(M, N, K, fmt, seed=31)
+    D = tcx.gemm(A, B, C)
+    C2 = C.clone()
+    tcx.gemm(A, B, C2, C2)
+    torch.cuda.synchronize()
+    assert torch.equal(D.view(torch.int32), C2.view(torch.int32))
+
+
+def test_gemm_bad_tile_n_rejected():
+    A, B, C = _problem(256, 256, 64, "bf16", seed=1)
+    with pytest.raises(tcx.TcxError):
+        tcx.gemm(A, B, C, tile_n=384)

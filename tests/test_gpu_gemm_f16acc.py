@@ -86,3 +86,13 @@ def test_f16acc_gemm_c3_shape_sampled():
     rows, cols = gemm_sample_coords(M, N, 256, 256, nsamp=16384, seed=3)
     worst = _check(A, B, C, D, rows, cols)
     assert worst > 0            # FP16 accumulation is inexact at this K (reported, within the bar)
+
+
+def test_f16acc_gemm_in_place():
+    M, N, K = 512, 512, 256
+    A, B, C = _problem(M, N, K, 41)
+    D = tcx.gemm(A, B, C, f16_acc=True)
+    C2 = C.clone()
+    tcx.gemm(A, B, C2, C2, f16_acc=True)
+    torch.cuda.synchronize()
+    assert torch.equal(D.view(torch.int16), C2.view(torch.int16))

@@ -162,3 +162,16 @@ def test_config5_full_size():
     mag = Ad.abs() @ Bd.abs().T
     err = (D[blk].double() - ref64).abs()
     assert bool((err <= (K + 2) * 2.0 ** -23 * mag + K * 2.0 ** -52 * mag).all())
+
+
+def test_sparse_in_place_d_aliases_c():
+    M, N, K = 512, 480, 512
+    vals, meta, _ = _dense_24(M, K, 13)
+    B = tcxgen.normal_matrix((N, K), "f16", 13, tcxgen.STREAM_B, DEV)
+    C = tcxgen.normal_matrix((M, N), "f32", 13, tcxgen.STREAM_C, DEV)
+    hw = tcx.sp24_pack_meta(meta, M, K)
+    D = tcx.gemm_sp24(vals, hw, B, C)
+    C2 = C.clone()
+    tcx.gemm_sp24(vals, hw, B, C2, C2)
+    torch.cuda.synchronize()
+    assert torch.equal(D.view(torch.int32), C2.view(torch.int32))
