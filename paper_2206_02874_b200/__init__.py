@@ -225,7 +225,7 @@ def sp24_pack_meta(meta_canon, M, K, ab=F16, check=True):
     return hw
 
 
-def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m=0, tf32=False):
+def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m=0, tf32=False, tile_m=0):
     """D = expand(vals, meta) x B + C; vals (M, K/2), B (N, K).  FP16/BF16 -> FP32, INT8 -> INT32
     (meta_hw packed with the same ab: sp24_pack_meta(meta, M, K, ab=S8) for int8)."""
     _dev_check(vals, meta_hw, B, C, D)
@@ -235,7 +235,7 @@ def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m
     cd = S32 if ab == S8 else F32
     if D is None:
         D = torch.empty((M, N), dtype=torch.int32 if cd == S32 else torch.float32, device=vals.device)
-    opts = GemmOpts(cta_group, max_ctas, group_m)
+    opts = GemmOpts(cta_group, max_ctas, group_m, 512 if tile_m == 512 else 0)
     _check(lib().tcx_gemm_sp24_ex(ab, cd, M, N, K, _ptr(vals), vals.stride(0), _ptr(meta_hw), _ptr(B), B.stride(0),
                                   _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
                                   ctypes.byref(opts), _stream(vals)))

@@ -286,6 +286,7 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
     if (opts->cta_group == 1 || opts->cta_group == 2) g.cta_group = opts->cta_group;
     g.max_ctas = opts->max_ctas;
     g.group_m = opts->group_m;
+    g.tile_n = opts->tile_n;
   }
   if (g.cta_group == 2 && M % 256)
     return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: the CTA-pair kernel needs M %% 256 == 0 (use cta_group=1)");

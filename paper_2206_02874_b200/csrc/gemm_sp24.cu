@@ -27,30 +27,40 @@ constexpr int BN = 240;            // UMMA N
 constexpr int NUM_THREADS = 256;
 constexpr int EPI_WARPS = 4;
 constexpr int GROUP_M = 8;            // default raster group (cluster-tile rows sweeping N together)
-template <int CG, int KIND>
+// MW = 1 ("M-wide", CTA pair tile 512 x 240): two M-halves share each stage's B (30 of the 48 KiB a
+// stage moves), so a stage carries 66 KiB for twice the work — 31% fewer operand bytes per FLOP
+// into each SM, whose TMA ingress the 2:4 stream otherwise saturates.  Both halves'
+// accumulators fill TMEM (2 x 240 columns + the metadata ring), so the accumulator is
+// single-buffered: per-half empty barriers and a half-0 lookahead as in gemm_dense.cu's wide tile.
+template <int CG, int KIND, int MW = 0>
 struct SpCfg {
+  static constexpr int MH = MW ? 2 : 1;                    // M-halves per tile (accumulators)
   static constexpr int ES = KIND == KIND_I8 ? 1 : KIND == KIND_TF32 ? 4 : 2;   // element bytes
   static constexpr int KL = 256 / ES;                      // logical K per stage (= 128 B of kept A)
   static constexpr int BOX = 128 / ES;                     // elements per 128-byte SW128 box row
-  // 2 KiB metadata atoms per stage (one atom = 128 rows x 128 logical 8/16-bit K; a TF32 element
-  // counts as two 16-bit halves, so a 64-logical-K TF32 stage is one atom)
+  // 2 KiB metadata atoms per stage and M-half (one atom = 128 rows x 128 logical 8/16-bit K; a TF32
+  // element counts as two 16-bit halves, so a 64-logical-K TF32 stage is one atom)
   static constexpr int META_ATOMS = KIND == KIND_TF32 ? 1 : KL / 128;
-  static constexpr int META_BYTES = 2048 * META_ATOMS;
-  static constexpr int META_COLS = 4 * META_ATOMS;         // TMEM columns per stage
-  static constexpr int MMA_COLS = META_COLS / 4;           // metadata columns read by one MMA
+  static constexpr int META_BYTES = 2048 * META_ATOMS * MH;
+  static constexpr int META_COLS = 4 * META_ATOMS * MH;    // TMEM columns per stage
   static constexpr int BN_LOAD = BN / CG;
-  static constexpr int A_BYTES = BM * 128;                 // 128 bytes of kept values per row
+  static constexpr int A_HALF = BM * 128;                  // 128 bytes of kept values per row
+  static constexpr int A_BYTES = A_HALF * MH;
   static constexpr int B_HALF = BN_LOAD * 128;             // one SW128 box (128 bytes of K per row)
   static constexpr int B_BYTES = 2 * B_HALF;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + META_BYTES;
-  static constexpr int STAGES = CG == 1 ? 2 : 4;
+  static constexpr int STAGES = CG == 1 ? 2 : (MW ? 3 : 4);
+  static constexpr int TILE_M = BM * CG * MH;
   static constexpr int SMEM_DATA = STAGES * STAGE_BYTES;
   static constexpr int STG_BYTES = EPI_WARPS * 2 * 2048;   // epilogue: 2 x 2 KiB (32 rows x 16 cols) per warp
   static constexpr int SMEM_TOTAL = SMEM_DATA + STG_BYTES + 1024 + 1024;
   static constexpr int META_COL = 512 - STAGES * META_COLS;    // metadata ring at the top of TMEM
-  static constexpr int ACC_STRIDE = KIND == KIND_I8 ? BN : 256;   // second accumulator's column
+  // accumulator columns: MW -> M-half h at h * BN (one buffer); else buffer b at b * ACC_STRIDE
+  static constexpr int ACC_STRIDE = MW ? BN : (KIND == KIND_I8 ? BN : 256);
   static_assert(B_HALF % 1024 == 0, "SW128 atoms need 1 KiB alignment");
   static_assert(ACC_STRIDE + BN <= META_COL, "TMEM budget");
+  static_assert(!MW || (CG == 2 && KIND != KIND_I8), "M-wide sparse tiles: CTA pair, f16/bf16/tf32");
+  static_assert(SMEM_TOTAL <= 232448, "smem budget");
 };
 
 struct Smem {
@@ -73,14 +83,15 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64
   nt = r / gm;
 }
 
-template <int CG, int KIND>
+template <int CG, int KIND, int MW>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmC,
                  const __grid_constant__ CUtensorMap tmD, int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc,
                  int group_m) {
-  using C_ = SpCfg<CG, KIND>;
+  using C_ = SpCfg<CG, KIND, MW>;
   constexpr int KL = C_::KL;
+  constexpr int MH = C_::MH;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem* sm = (Smem*)(smem + C_::SMEM_DATA + C_::STG_BYTES);
@@ -88,7 +99,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int warp = threadIdx.x / 32;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
-  const int64_t m_tiles = M / (BM * CG);
+  const int64_t m_tiles = M / C_::TILE_M;
   const int64_t n_tiles = (N + BN - 1) / BN;
   const int64_t num_tiles = m_tiles * n_tiles;
   const int64_t k_blocks = K / KL;
@@ -115,9 +126,8 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int64_t mt, nt;
         tile_coords(tile, m_tiles, n_tiles, group_m, mt, nt);
-        const int64_t mrow = mt * BM * CG + rank * BM;
+        const int64_t mrow = mt * C_::TILE_M + rank * BM;            // + h * BM * CG for M-half h
         const int brow = (int)(nt * BN + rank * C_::BN_LOAD);
-        const int64_t mb = mrow / 128;
         for (int64_t kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&sm->empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C_::STAGE_BYTES;
@@ -125,21 +135,24 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           uint8_t* se = sb + C_::B_BYTES;
           const int ka = (int)(kb * (KL / 2));     // kept-value column
           const int kx = (int)(kb * KL);           // logical column of B
-          const int erow = (int)((mb * k_blocks + kb) * 16 * C_::META_ATOMS);
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&sm->full[stage], C_::STAGE_BYTES);
-            tma_load_2d(sa, &tmA, &sm->full[stage], ka, (int)mrow);
-            tma_load_2d(sb, &tmB, &sm->full[stage], kx, brow);
-            tma_load_2d(sb + C_::B_HALF, &tmB, &sm->full[stage], kx + C_::BOX, brow);
-            tma_load_2d(se, &tmE, &sm->full[stage], 0, erow);
           } else {
             if (leader) mbar_arrive_expect_tx(&sm->full[stage], 2 * C_::STAGE_BYTES);
-            const uint32_t bar = full0_cluster + stage * 8;
-            tma_load_2d_cg2(sa, &tmA, bar, ka, (int)mrow);
-            tma_load_2d_cg2(sb, &tmB, bar, kx, brow);
-            tma_load_2d_cg2(sb + C_::B_HALF, &tmB, bar, kx + C_::BOX, brow);
-            tma_load_2d_cg2(se, &tmE, bar, 0, erow);
           }
+          const uint32_t bar = CG == 2 ? full0_cluster + stage * 8 : smem_u32(&sm->full[stage]);
+          auto load = [&](void* dst, const CUtensorMap* m, int x, int y) {
+            if constexpr (CG == 1) tma_load_2d(dst, m, &sm->full[stage], x, y);
+            else tma_load_2d_cg2(dst, m, bar, x, y);
+          };
+#pragma unroll
+          for (int h = 0; h < MH; ++h) {
+            const int64_t mrow_h = mrow + h * BM * CG;
+            load(sa + h * C_::A_HALF, &tmA, ka, (int)mrow_h);
+            load(se + h * 2048 * C_::META_ATOMS, &tmE, 0, (int)(((mrow_h / 128) * k_blocks + kb) * 16 * C_::META_ATOMS));
+          }
+          load(sb, &tmB, kx, brow);
+          load(sb + C_::B_HALF, &tmB, kx + C_::BOX, brow);
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -148,42 +161,76 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     if (leader) {
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t acc_phase = 0;
+      // stage `st`, M-half h: metadata atoms -> TMEM (in order before the MMAs), then 4 sparse MMAs
+      auto issue = [&](int st, int h, int64_t kb, uint32_t tmem_d) {
+        const uint32_t sa = smem_u32(smem + st * C_::STAGE_BYTES) + h * C_::A_HALF;
+        const uint32_t sb = smem_u32(smem + st * C_::STAGE_BYTES) + C_::A_BYTES;
+        const uint32_t se = sb + C_::B_BYTES + h * 2048 * C_::META_ATOMS;
+        const uint32_t tmeta = tmem_base + C_::META_COL + st * C_::META_COLS + h * 4 * C_::META_ATOMS;
+#pragma unroll
+        for (int a = 0; a < C_::META_ATOMS; ++a) tc05_cp_128x128b<CG>(tmeta + 4 * a, sdesc(se + 2048 * a, 128, 128, 0));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          // MMA j: 32 bytes of kept A (K/2 logical), 64 bytes of B (one half of a SW128 box row)
+          const uint64_t ad = sdesc(sa + j * 32, 16, 1024, 2);
+          const uint64_t bd = sdesc(sb + (j >> 1) * C_::B_HALF + (j & 1) * 64, 16, 1024, 2);
+          if constexpr (KIND == KIND_I8) {
+            const uint32_t e = tmeta + 2 * j;          // 2 columns per MMA, selector 0
+            umma_sp<CG, KIND_I8>(tmem_d, ad, bd, e, idesc, (kb | j) ? 1u : 0u);
+          } else {
+            const uint32_t e = tmeta + j;              // low address bit -> sparse selector
+            umma_sp<CG, KIND>(tmem_d, ad, bd, e & ~1u, idesc | (e & 1u), (kb | j) ? 1u : 0u);
+          }
+        }
+      };
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        if constexpr (CG == 2) mbar_wait_cluster(&sm->tmem_empty[acc], acc_phase ^ 1);
-        else mbar_wait(&sm->tmem_empty[acc], acc_phase ^ 1);
-        tc05_fence_after();
+        int64_t kb0 = 0;
+        if constexpr (!MW) {
+          if constexpr (CG == 2) mbar_wait_cluster(&sm->tmem_empty[acc], acc_phase ^ 1);
+          else mbar_wait(&sm->tmem_empty[acc], acc_phase ^ 1);
+          tc05_fence_after();
+        } else {
+          // single buffer: half 0 for the first L resident stages while half 1 still drains
+          const int64_t L = k_blocks < C_::STAGES ? k_blocks : C_::STAGES;
+          const int st0 = stage;
+          mbar_wait_cluster(&sm->tmem_empty[0], acc_phase ^ 1);
+          tc05_fence_after();
+          for (int64_t kb = 0; kb < L; ++kb) {
+            mbar_wait(&sm->full[stage], phase);
+            tc05_fence_after();
+            if (elect_one()) issue(stage, 0, kb, tmem_base);
+            __syncwarp();
+            if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
+          }
+          mbar_wait_cluster(&sm->tmem_empty[1], acc_phase ^ 1);
+          tc05_fence_after();
+          int st = st0;
+          for (int64_t kb = 0; kb < L; ++kb) {
+            if (elect_one()) {
+              issue(st, 1, kb, tmem_base + BN);
+              tc05_commit<CG>(&sm->empty[st]);
+              if (kb == k_blocks - 1) tc05_commit<CG>(&sm->tmem_full[0]);
+            }
+            __syncwarp();
+            if (++st == C_::STAGES) st = 0;
+          }
+          kb0 = L;
+        }
         const uint32_t tmem_d = tmem_base + acc * C_::ACC_STRIDE;
-        for (int64_t kb = 0; kb < k_blocks; ++kb) {
+        for (int64_t kb = kb0; kb < k_blocks; ++kb) {
           mbar_wait(&sm->full[stage], phase);
           tc05_fence_after();
           if (elect_one()) {
-            const uint32_t sa = smem_u32(smem + stage * C_::STAGE_BYTES);
-            const uint32_t sb = sa + C_::A_BYTES;
-            const uint32_t se = sb + C_::B_BYTES;
-            const uint32_t tmeta = tmem_base + C_::META_COL + stage * C_::META_COLS;
-            // metadata atoms -> TMEM (128 lanes x 16 B each); execute in order before the MMAs below
 #pragma unroll
-            for (int h = 0; h < C_::META_ATOMS; ++h) tc05_cp_128x128b<CG>(tmeta + 4 * h, sdesc(se + 2048 * h, 128, 128, 0));
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              // MMA j: 32 bytes of kept A (K/2 logical), 64 bytes of B (one half of a SW128 box row)
-              const uint64_t ad = sdesc(sa + j * 32, 16, 1024, 2);
-              const uint64_t bd = sdesc(sb + (j >> 1) * C_::B_HALF + (j & 1) * 64, 16, 1024, 2);
-              if constexpr (KIND == KIND_I8) {
-                const uint32_t e = tmeta + 2 * j;          // 2 columns per MMA, selector 0
-                umma_sp<CG, KIND_I8>(tmem_d, ad, bd, e, idesc, (kb | j) ? 1u : 0u);
-              } else {
-                const uint32_t e = tmeta + j;              // low address bit -> sparse selector
-                umma_sp<CG, KIND>(tmem_d, ad, bd, e & ~1u, idesc | (e & 1u), (kb | j) ? 1u : 0u);
-              }
-            }
+            for (int h = 0; h < MH; ++h) issue(stage, h, kb, MW ? tmem_base + h * BN : tmem_d);
             tc05_commit<CG>(&sm->empty[stage]);
             if (kb == k_blocks - 1) tc05_commit<CG>(&sm->tmem_full[acc]);
           }
           __syncwarp();
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
         }
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (MW) { acc_phase ^= 1; }
+        else if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else if (warp >= 4) {
@@ -193,7 +240,8 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     // alternate, the C chunk two ahead loading while this one is stored (as in gemm_dense.cu).
     const int e = warp - 4;
     const int lane = threadIdx.x & 31;
-    constexpr int CH = BN / 16;
+    constexpr int HCH = BN / 16;                 // chunks per accumulator (M-half)
+    constexpr int CH = HCH * MH;                 // chunks per tile
     uint8_t* stg = smem + C_::SMEM_DATA + e * 4096;
     uint64_t* cbar = &sm->cbar[e][0];
     uint32_t cph[2] = {0u, 0u};
@@ -203,8 +251,9 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     auto coords = [&](int64_t q, int& x, int& y) {
       int64_t mt, nt;
       tile_coords(cluster_id + (q / CH) * num_clusters, m_tiles, n_tiles, group_m, mt, nt);
-      y = (int)(mt * BM * CG + rank * BM + e * 32);
-      x = (int)(nt * BN + (q % CH) * 16);
+      const int ch = (int)(q % CH);
+      y = (int)(mt * C_::TILE_M + (ch / HCH) * BM * CG + rank * BM + e * 32);
+      x = (int)(nt * BN + (ch % HCH) * 16);
     };
     auto load_c = [&](int64_t q) {
       if (has_c && lane == 0 && q < nq) {
@@ -221,7 +270,9 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       mbar_wait(&sm->tmem_full[acc], acc_phase);
       tc05_fence_after();
       uint32_t v[16], vn[16];
-      tmem_ld_32x32b_x16(tmem_base + acc * C_::ACC_STRIDE + lane_off, vn);
+      // chunk ch lives at column (M-half) * BN + (ch % HCH) * 16 (MW) or acc * ACC_STRIDE + ch * 16
+      auto tcol = [&](int ch) { return tmem_base + (MW ? (ch / HCH) * BN : acc * C_::ACC_STRIDE) + (ch % HCH) * 16 + lane_off; };
+      tmem_ld_32x32b_x16(tcol(0), vn);
 #pragma unroll 1
       for (int ch = 0; ch < CH; ++ch) {
         const int64_t q = it * CH + ch;
@@ -229,11 +280,12 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = vn[j];
-        if (ch + 1 < CH) tmem_ld_32x32b_x16(tmem_base + acc * C_::ACC_STRIDE + (ch + 1) * 16 + lane_off, vn);
-        if (ch == CH - 1) {
+        if (ch + 1 < CH) tmem_ld_32x32b_x16(tcol(ch + 1), vn);
+        if (ch % HCH == HCH - 1) {
+          // accumulator part read: MW -> M-half ch / HCH of the single buffer; else buffer `acc`
           tc05_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(tmem_empty_cluster + acc * 8);
+          if (lane == 0) mbar_arrive_cluster(tmem_empty_cluster + (MW ? ch / HCH : acc) * 8);
         }
         if (has_c) {
           mbar_wait(&cbar[b], cph[b]);
@@ -270,7 +322,8 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
         load_c(q + 2);
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (MW) { acc_phase ^= 1; }
+      else if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) bulk_wait<0>();
   }
@@ -280,10 +333,10 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (warp == 2) { tc05_fence_after(); tmem_dealloc<CG>(tmem_base, 512); }
 }
 
-template <int CG, int KIND>
+template <int CG, int KIND, int MW = 0>
 tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
-  using C_ = SpCfg<CG, KIND>;
-  if (a.M % (BM * CG)) return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: M %% %d != 0", BM * CG);
+  using C_ = SpCfg<CG, KIND, MW>;
+  if (a.M % C_::TILE_M) return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: M %% %d != 0", C_::TILE_M);
   const CUtensorMapDataType dt = KIND == KIND_I8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                  : KIND == KIND_TF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                  : a.ab == TCX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
@@ -310,9 +363,9 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   } else {
     tC = tD;
   }
-  auto kern = gemm_sp24_kernel<CG, KIND>;
+  auto kern = gemm_sp24_kernel<CG, KIND, MW>;
   TCX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_TOTAL));
-  const int64_t tiles = (a.M / (BM * CG)) * ((a.N + BN - 1) / BN);
+  const int64_t tiles = (a.M / C_::TILE_M) * ((a.N + BN - 1) / BN);
   int64_t clusters = tiles;
   int64_t max_clusters = dev.sm_count / CG;
   if (a.max_ctas > 0 && a.max_ctas / CG < max_clusters) max_clusters = a.max_ctas / CG > 0 ? a.max_ctas / CG : 1;
@@ -342,8 +395,13 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
 
 tcx_status launch_gemm_sp24(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   if (a.ab == TCX_S8) return a.cta_group == 1 ? launch_sp<1, KIND_I8>(a, dev, s) : launch_sp<2, KIND_I8>(a, dev, s);
-  if (a.ab == TCX_TF32) return a.cta_group == 1 ? launch_sp<1, KIND_TF32>(a, dev, s) : launch_sp<2, KIND_TF32>(a, dev, s);
-  return a.cta_group == 1 ? launch_sp<1, KIND_F16>(a, dev, s) : launch_sp<2, KIND_F16>(a, dev, s);
+  // tile_m = 512 (opts.tile_n field reused as the sparse tile height): the M-wide pair tile
+  const bool mw = a.tile_n == 512 && a.cta_group != 1 && a.M % 512 == 0;
+  if (a.ab == TCX_TF32)
+    return a.cta_group == 1 ? launch_sp<1, KIND_TF32>(a, dev, s)
+                            : (mw ? launch_sp<2, KIND_TF32, 1>(a, dev, s) : launch_sp<2, KIND_TF32>(a, dev, s));
+  return a.cta_group == 1 ? launch_sp<1, KIND_F16>(a, dev, s)
+                          : (mw ? launch_sp<2, KIND_F16, 1>(a, dev, s) : launch_sp<2, KIND_F16>(a, dev, s));
 }
 
 }  // namespace tcx

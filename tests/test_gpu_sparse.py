@@ -175,3 +175,36 @@ def test_sparse_in_place_d_aliases_c():
     tcx.gemm_sp24(vals, hw, B, C2, C2)
     torch.cuda.synchronize()
     assert torch.equal(D.view(torch.int32), C2.view(torch.int32))
+
+
+@pytest.mark.parametrize("shape", [(512, 240, 128), (1024, 496, 640), (1536, 1024, 1024)])
+def test_sparse_m_wide_tile_vs_oracle_and_narrow(shape):
+    """the 512 x 240 pair tile (tile_m = 512: two M-halves share B and the stage) vs the oracle, and
+    bit-identical to the 256 x 240 tile (same MMA sequence per output element)."""
+    M, N, K = shape
+    vals, meta, _ = _dense_24(M, K, M + 7 * N + K)
+    B = tcxgen.normal_matrix((N, K), "f16", M + N, tcxgen.STREAM_B, DEV)
+    C = tcxgen.normal_matrix((M, N), "f32", M + N, tcxgen.STREAM_C, DEV)
+    hw = tcx.sp24_pack_meta(meta, M, K)
+    Dw = tcx.gemm_sp24(vals, hw, B, C, tile_m=512)
+    Dn = tcx.gemm_sp24(vals, hw, B, C)
+    Dp = tcx.gemm_sp24(vals, hw, B, C, tile_m=512, max_ctas=2)
+    torch.cuda.synchronize()
+    assert torch.equal(Dw.view(torch.int32), Dn.view(torch.int32))
+    assert torch.equal(Dw.view(torch.int32), Dp.view(torch.int32))
+    ii, jj = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+    ref, absv = O.gemm_samples(O.F16, O.sp24_expand(host_bits(vals), host_bits(meta), K), host_bits(B),
+                               host_bits(C), ii.ravel(), jj.ravel())
+    fp_bound_check(host_bits(Dw).ravel(), ref, absv, K, f"sp24 mwide {shape}")
+
+
+def test_sparse_m_wide_integer_bit_exact_bf16():
+    M, N, K = 1024, 480, 1024
+    vals, meta, dense = _dense_24(M, K, 15, torch.bfloat16, integer=True)
+    B = tcxgen.int32_matrix((N, K), 15, 2, -8, 8, DEV).to(torch.bfloat16)
+    C = tcxgen.int32_matrix((M, N), 15, 3, -1000, 1000, DEV).to(torch.float32)
+    hw = tcx.sp24_pack_meta(meta, M, K, ab=tcx.BF16)
+    D = tcx.gemm_sp24(vals, hw, B, C, tile_m=512)
+    ref = dense.double() @ B.double().T + C.double()
+    torch.cuda.synchronize()
+    assert torch.equal(D.double(), ref)

@@ -113,3 +113,15 @@ def test_tf32_sparse_equals_dense_of_expanded():
     Dd = tcx.gemm(dense, B, None, tf32=True)
     torch.cuda.synchronize()
     assert torch.equal(Ds, Dd)
+
+
+def test_tf32_sparse_m_wide_bit_exact():
+    M, N, K = 1024, 480, 512
+    dense = _sparse12(M, K, 9, integer=True)
+    vals, meta = tcx.sp24_compress(dense, tf32=True)
+    B = tcxgen.int32_matrix((N, K), 9, 2, -8, 8, DEV).to(torch.float32)
+    hw = tcx.sp24_pack_meta(meta, M, K, ab=tcx.TF32)
+    D = tcx.gemm_sp24(vals, hw, B, None, tf32=True, tile_m=512)
+    ref = dense.double() @ B.double().T
+    torch.cuda.synchronize()
+    assert torch.equal(D.double(), ref)

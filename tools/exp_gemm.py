@@ -2,7 +2,7 @@
 """Kernel-configuration sweep for the GEMM paths (raster group, CTA mode).
 
 usage: python tools/exp_gemm.py c5|c3|c4|c3tf32 [steps] [variant ...]
-variant = "g<group_m>c<cta_group>" e.g. g8c2, g16c2, g8c1.  Prints one JSON line per variant
+variant = "g<group_m>c<cta_group>[w]" e.g. g8c2, g16c2, g8c1, g8c2w (w = the 512-wide tile).  Prints one JSON line per variant
 with device time (CUDA events), TFLOP/s, NVML SM clock / power during the run, and whether D is
 bit-identical to the first variant's D (the knobs change no arithmetic)."""
 import json
@@ -20,8 +20,11 @@ import bench  # noqa: E402
 
 
 def parse(v):
-    m = re.fullmatch(r"g(\d+)c(\d)", v)
-    return dict(group_m=int(m.group(1)), cta_group=int(m.group(2)))
+    m = re.fullmatch(r"g(\d+)c(\d)(w?)", v)
+    kw = dict(group_m=int(m.group(1)), cta_group=int(m.group(2)))
+    if m.group(3):
+        kw["wide"] = True
+    return kw
 
 
 def main():
@@ -41,10 +44,11 @@ def main():
     ref = None
     for v in variants:
         kw = parse(v)
+        wide = kw.pop("wide", False)
         if cfg == "c5":
-            step = lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, **kw)
+            step = lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, tile_m=512 if wide else 0, **kw)
         else:
-            step = lambda: tcx.gemm(w.A, w.B, w.C, w.D, tf32=getattr(w, "tf32", False), **kw)
+            step = lambda: tcx.gemm(w.A, w.B, w.C, w.D, tf32=getattr(w, "tf32", False), tile_n=512 if wide else 0, **kw)
         for _ in range(3):
             step()
         torch.cuda.synchronize()
