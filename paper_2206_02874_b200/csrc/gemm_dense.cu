@@ -88,12 +88,14 @@ template <int CG, int KIND, int NH>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
-                  int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc, int group_m) {
+                  int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc, int group_m,
+                  uint32_t stagger_ns) {
   using C_ = Cfg<CG, NH>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem* sm = (Smem*)(smem + C_::SMEM_DATA + C_::STG_BYTES);
 
+  const uint64_t t_start = global_ns();
   const int warp = threadIdx.x / 32;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
@@ -121,6 +123,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   if (warp == 0) {
     // ================= TMA producer =================
     if (elect_one()) {
+      stagger_start(t_start, cluster_id, stagger_ns);
       int stage = 0; uint32_t phase = 0;
       const uint32_t full0_cluster = CG == 2 ? mapa(smem_u32(&sm->full[0]), 0) : 0;
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
@@ -340,11 +343,19 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         tma_load_2d(stg + (q & 1) * 4096, &tmC, &cbar[q & 1], x, y);
       }
     };
+    // single-buffered (wide) tiles: the epilogue is on the critical path, so each tile's C is
+    // L2-prefetched a tile ahead and its chunk loads hit L2 (double-buffered tiles hide the latency)
+    auto prefetch_c_tile = [&](int64_t it) {
+      if (NH == 2 && has_c && lane == 0 && it < my_tiles)
+        for (int ch = 0; ch < CH; ++ch) { int x, y; coords(it * CH + ch, x, y); tma_prefetch_2d(&tmC, x, y); }
+    };
+    prefetch_c_tile(0);
     load_c(0);
     load_c(1);
     int acc = 0; uint32_t acc_phase = 0;
     const uint32_t lane_off = (uint32_t)(e * 32) << 16;
     for (int64_t it = 0; it < my_tiles; ++it) {
+      prefetch_c_tile(it + 1);
       mbar_wait(&sm->tmem_full[acc], acc_phase);
       tc05_fence_after();
       uint32_t v[32], vn[32];
@@ -468,7 +479,10 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
   cfg.attrs = attr; cfg.numAttrs = 1;
   const uint32_t idesc = make_idesc(KIND, a_fmt, BM * CG, BN);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
-                                  a.C ? 1 : 0, idesc, a.group_m > 0 ? a.group_m : GROUP_M));
+                                  a.C ? 1 : 0, idesc, a.group_m > 0 ? a.group_m : GROUP_M,
+                                  NH == 2 ? wide_stagger_ns(2.0 * C_::TILE_M * C_::TILE_N * (double)a.K,
+                                                            22938.0 * (KIND == KIND_TF32 ? 0.5 : KIND == KIND_I8 ? 2.0 : 1.0))
+                                          : 0u));
   count_launch();
   return TCX_OK;
 }
