@@ -279,3 +279,24 @@ def ldmatrix(num: int, trans: bool, smem_u16: np.ndarray, row_elem: np.ndarray) 
             lo, hi = (M[g][2 * t], M[g][2 * t + 1]) if not trans else (M[2 * t][g], M[2 * t + 1][g])
             out[l, j] = lo | (hi << 16)
     return out
+
+
+# ---------------------------------------------------------------------------- TF32 input conversion
+def tf32_convert(bits32: np.ndarray, mode: str) -> np.ndarray:
+    """How FP32 storage may become a TF32 operand (SURVEY §8(c) reading C1: the paper never says;
+    C2's raw-input sub-class observes it).  Element-wise on FP32 bits, finite inputs:
+      "rz"  drop the low 13 significand bits (truncation toward zero);
+      "rne" round to nearest, ties to even (quantize(x, TF32));
+      "rna" round to nearest, ties away from zero (add half a TF32 ulp to the magnitude, then drop
+            the low 13 bits: PTX cvt.rna.tf32.f32);
+      "fp32" keep every bit (the tensor core reads FP32)."""
+    b = np.asarray(bits32, dtype=np.uint32)
+    if mode == "fp32":
+        return b.copy()
+    if mode == "rz":
+        return b & np.uint32(0xFFFFE000)
+    if mode == "rna":
+        return (b + np.uint32(0x1000)) & np.uint32(0xFFFFE000)     # sign bit untouched for finite values
+    if mode == "rne":
+        return quantize_f32_bits(b, TF32).astype(np.uint32)
+    raise ValueError(mode)

@@ -77,12 +77,6 @@ tcx_status make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* ba
   return TCX_OK;
 }
 
-uint32_t wide_stagger_ns(double tile_flops, double flop_per_ns) {
-  static double scale = [] { const char* e = getenv("TCX_STAGGER"); return e ? atof(e) : 0.0; }();
-  const double ns = scale * tile_flops / flop_per_ns;
-  return ns <= 0 ? 0u : (ns > 4e9 ? 4000000000u : (uint32_t)ns);
-}
-
 static int esize_of(tcx_dtype t) {
   switch (t) {
     case TCX_F16: case TCX_BF16: return 2;

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmC,
                  const __grid_constant__ CUtensorMap tmD, int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc,
-                 int group_m, uint32_t stagger_ns) {
+                 int group_m) {
   using C_ = SpCfg<CG, KIND, MW>;
   constexpr int KL = C_::KL;
   constexpr int MH = C_::MH;
@@ -96,7 +96,6 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem* sm = (Smem*)(smem + C_::SMEM_DATA + C_::STG_BYTES);
 
-  const uint64_t t_start = global_ns();
   const int warp = threadIdx.x / 32;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
@@ -122,7 +121,6 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
   if (warp == 0) {
     if (elect_one()) {
-      stagger_start(t_start, cluster_id, stagger_ns);
       int stage = 0; uint32_t phase = 0;
       const uint32_t full0_cluster = CG == 2 ? mapa(smem_u32(&sm->full[0]), 0) : 0;
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
@@ -396,10 +394,7 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   const uint32_t idesc = (1u << 2) | (cfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
                          ((uint32_t)((BM * CG) >> 4) << 24);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tE, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
-                                  a.C ? 1 : 0, idesc, a.group_m > 0 ? a.group_m : GROUP_M,
-                                  MW ? wide_stagger_ns(2.0 * C_::TILE_M * BN * (double)a.K,
-                                                       22938.0 * 1.78 * (KIND == KIND_TF32 ? 0.5 : 1.0))
-                                     : 0u));
+                                  a.C ? 1 : 0, idesc, a.group_m > 0 ? a.group_m : GROUP_M));
   count_launch();
   return TCX_OK;
 }

@@ -277,17 +277,6 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ------------------------------------------------------------------ misc
-__device__ __forceinline__ uint64_t global_ns() {
-  uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
-}
-// Single-buffered (wide) tiles drain their accumulators between tiles; if every cluster does so
-// at once, the epilogues' C/D traffic bursts at HBM together.  Staggering each cluster's start by
-// (cluster % 8)/8 of a tile's time spreads the drains out (the offsets persist: clusters run alike).
-__device__ __forceinline__ void stagger_start(uint64_t t0, int64_t cluster_id, uint32_t stagger_ns) {
-  if (stagger_ns == 0) return;
-  const uint64_t until = t0 + (uint64_t)(cluster_id % 8) * (stagger_ns / 8);
-  while (global_ns() < until) __nanosleep(256);
-}
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
 }

@@ -56,9 +56,6 @@ struct GemmArgs {
   int tile_n;     // dense: 256 / 512 / 0 = auto
 };
 tcx_status launch_gemm_dense(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);
-// start-stagger for single-buffered wide tiles: estimated tile time (ns) from its dense-equivalent
-// FLOPs at `flop_per_ns` per CTA pair; TCX_STAGGER (env, experiment) scales it (0 = off)
-uint32_t wide_stagger_ns(double tile_flops, double flop_per_ns);
 tcx_status launch_gemm_sp24(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);
 tcx_status launch_fill_c(const GemmArgs& a, cudaStream_t s);   // K == 0: D = C (or 0)
 

@@ -117,3 +117,22 @@ def test_round_toward_zero_bound():
     for x in _random_doubles(rng, 3000, -20, 20).tolist():
         for fmt in (O.F16, O.BF16, O.TF32, O.F32):
             assert abs(O.decode(fmt, O.quantize(x, fmt, rz=True))) <= abs(x)
+
+
+def test_tf32_convert_modes_closed_form():
+    """TF32 input conversions (reading C1): ulp(1) in TF32 = 2^-10; 1 + 2^-11 is a tie."""
+    import struct
+    def b(x):
+        return np.array([struct.unpack("<I", struct.pack("<f", x))[0]], np.uint32)
+    def f(u):
+        return struct.unpack("<f", struct.pack("<I", int(u[0])))[0]
+    tie, above, below = 1 + 2.0 ** -11, 1 + 2.0 ** -11 + 2.0 ** -20, 1 + 2.0 ** -11 - 2.0 ** -20
+    odd_tie = 1 + 2.0 ** -10 + 2.0 ** -11
+    assert f(O.tf32_convert(b(tie), "rz")) == 1.0
+    assert f(O.tf32_convert(b(tie), "rne")) == 1.0
+    assert f(O.tf32_convert(b(tie), "rna")) == 1 + 2.0 ** -10
+    assert f(O.tf32_convert(b(odd_tie), "rne")) == 1 + 2.0 ** -9
+    assert f(O.tf32_convert(b(above), "rz")) == 1.0 and f(O.tf32_convert(b(above), "rne")) == 1 + 2.0 ** -10
+    assert f(O.tf32_convert(b(below), "rna")) == 1.0
+    assert f(O.tf32_convert(b(-tie), "rna")) == -(1 + 2.0 ** -10)
+    assert f(O.tf32_convert(b(0.7), "fp32")) == np.float32(0.7)
