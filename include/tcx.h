@@ -99,7 +99,13 @@ typedef struct {
   int tile_n;      /* 0 = library choice; 512: tcx_gemm's 256 x 512 pair tile (two N = 256 MMAs
                       share A), tcx_gemm_sp24's 512 x 240 pair tile (two M-halves share B;
                       F16/BF16/TF32, M % 512 == 0) */
-  int reserved[4];
+  int pairs_m;     /* CTA pair only (not with tile_n = 512): groups of pairs_m x pairs_n CTA pairs   */
+  int pairs_n;     /* compute adjacent pair tiles and are launched as preferred clusters; where the  */
+                   /* hardware forms the cluster, A (sA) is TMA-multicast across the pairs_n pairs  */
+                   /* of a row and B across the pairs_m pairs of a column; elsewhere the pairs load */
+                   /* their own operands.  1 or 2 each; 0 = default 1.  Results are bit-identical  */
+                   /* to the default.                                                               */
+  int reserved[2];
 } tcx_gemm_opts;
 tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
                        const void* A, int64_t lda, const void* B, int64_t ldb,

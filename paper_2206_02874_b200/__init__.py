@@ -44,7 +44,8 @@ class TcxError(RuntimeError):
 
 class GemmOpts(ctypes.Structure):
     _fields_ = [("cta_group", ctypes.c_int), ("max_ctas", ctypes.c_int), ("group_m", ctypes.c_int),
-                ("tile_n", ctypes.c_int), ("reserved", ctypes.c_int * 4)]
+                ("tile_n", ctypes.c_int), ("pairs_m", ctypes.c_int), ("pairs_n", ctypes.c_int),
+                ("reserved", ctypes.c_int * 2)]
 
 
 class ProbeConfig(ctypes.Structure):
@@ -170,9 +171,10 @@ def mma_chain(A0, Bs, tf32=False, Ds=None):
 
 
 # ---------------------------------------------------------------------------------------- GEMM
-def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, tile_n=0, f16_acc=False):
+def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, tile_n=0, f16_acc=False, pairs=(0, 0)):
     """Dense D = A x B + C with A (M, K), B stored (N, K) ("row.col"), C/D (M, N).
-    f16_acc: FP16 inputs with an FP16 accumulator (C, D float16; C is the MMA's C operand)."""
+    f16_acc: FP16 inputs with an FP16 accumulator (C, D float16; C is the MMA's C operand).
+    pairs = (pairs_m, pairs_n): TMA-multicast cluster of CTA pairs (tcx_gemm_opts)."""
     _dev_check(A, B, C, D)
     ab = ab_code(A, tf32)
     M, K = A.shape
@@ -182,7 +184,7 @@ def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, t
         raise ValueError("f16_acc: C must be float16")
     if D is None:
         D = torch.empty((M, N), dtype={S32: torch.int32, F16: torch.float16, F32: torch.float32}[cd], device=A.device)
-    opts = GemmOpts(cta_group, max_ctas, group_m, tile_n)
+    opts = GemmOpts(cta_group, max_ctas, group_m, tile_n, pairs[0], pairs[1])
     _check(lib().tcx_gemm_ex(ab, cd, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
                              _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
                              ctypes.byref(opts), _stream(A)))
@@ -225,7 +227,7 @@ def sp24_pack_meta(meta_canon, M, K, ab=F16, check=True):
     return hw
 
 
-def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m=0, tf32=False, tile_m=0):
+def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m=0, tf32=False, tile_m=0, pairs=(0, 0)):
     """D = expand(vals, meta) x B + C; vals (M, K/2), B (N, K).  FP16/BF16 -> FP32, INT8 -> INT32
     (meta_hw packed with the same ab: sp24_pack_meta(meta, M, K, ab=S8) for int8)."""
     _dev_check(vals, meta_hw, B, C, D)
@@ -235,7 +237,7 @@ def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m
     cd = S32 if ab == S8 else F32
     if D is None:
         D = torch.empty((M, N), dtype=torch.int32 if cd == S32 else torch.float32, device=vals.device)
-    opts = GemmOpts(cta_group, max_ctas, group_m, 512 if tile_m == 512 else 0)
+    opts = GemmOpts(cta_group, max_ctas, group_m, 512 if tile_m == 512 else 0, pairs[0], pairs[1])
     _check(lib().tcx_gemm_sp24_ex(ab, cd, M, N, K, _ptr(vals), vals.stride(0), _ptr(meta_hw), _ptr(B), B.stride(0),
                                   _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
                                   ctypes.byref(opts), _stream(vals)))

@@ -211,6 +211,13 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
     if (opts->tile_n != 0 && opts->tile_n != 256 && opts->tile_n != 512)
       return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: tile_n must be 0, 256 or 512");
     g.tile_n = opts->tile_n;
+    const int pm = opts->pairs_m ? opts->pairs_m : 1, pn = opts->pairs_n ? opts->pairs_n : 1;
+    if (pm < 1 || pm > 2 || pn < 1 || pn > 2)
+      return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: pairs_m and pairs_n must be 0, 1 or 2");
+    if ((pm > 1 || pn > 1) && (g.cta_group != 2 || g.tile_n == 512))
+      return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: multicast clusters need cta_group 2 and the 256-wide tile");
+    g.pairs_m = pm;
+    g.pairs_n = pn;
   }
   if (K == 0) return launch_fill_c(g, (cudaStream_t)stream);
   return launch_gemm_dense(g, dev, (cudaStream_t)stream);
@@ -287,6 +294,13 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
     g.max_ctas = opts->max_ctas;
     g.group_m = opts->group_m;
     g.tile_n = opts->tile_n;
+    const int pm = opts->pairs_m ? opts->pairs_m : 1, pn = opts->pairs_n ? opts->pairs_n : 1;
+    if (pm < 1 || pm > 2 || pn < 1 || pn > 2)
+      return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm_sp24: pairs_m and pairs_n must be 0, 1 or 2");
+    if ((pm > 1 || pn > 1) && (g.cta_group != 2 || g.tile_n == 512))
+      return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm_sp24: multicast groups need cta_group 2 and the 256-row tile");
+    g.pairs_m = pm;
+    g.pairs_n = pn;
   }
   if (g.cta_group == 2 && M % 256)
     return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: the CTA-pair kernel needs M %% 256 == 0 (use cta_group=1)");

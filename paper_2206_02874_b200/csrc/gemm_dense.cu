@@ -12,8 +12,21 @@
 // less L2->SM operand traffic per FLOP (the power-capped B200 turns that into clock); the two
 // halves fill all 512 TMEM columns, so the accumulator is single-buffered and the epilogue drains
 // half 0 first (its own empty barrier) so the next tile's half-0 MMAs can start early.
+// PM x PN > 1 (CG = 2, NH = 1): a group of PM x PN CTA pairs (CL = 2 PM PN consecutive CTAs)
+// computes a (256 PM) x (256 PN) block of adjacent pair tiles.  The pairs of a row need the same A
+// rows and the pairs of a column the same B rows, so when the group is one cluster each CTA
+// TMA-loads only a 1/PN slice of its A half and a 1/PM slice of its B half and multicasts it to the
+// CTAs that share it (same pair rank): L2->SM operand reads drop by (1/PN + 1/PM)/2 with the
+// 256 x 256 double-buffered accumulator kept, and every pair's commit of a smem slot arrives at
+// every CTA of the cluster (empty barriers count PM x PN arrivals).  Clusters of 4 / 8 CTAs must
+// sit inside one GPC and B200's GPCs fit fewer of them than 148 SMs (33 x 4, 15 x 8), so the
+// launch asks for CL-CTA clusters as the *preferred* shape over plain pairs: a group the hardware
+// could not place as one cluster runs as independent pairs (%cluster_nctarank == 2) on the same
+// tiles, loading every slice itself — every SM works, and the groups that did form multicast.
 // BK is one 128-byte swizzle row for every kind (64 f16/bf16, 32 tf32, 128 s8), and every
 // UMMA consumes 32 bytes of K (UMMA_K = 16 / 8 / 32).
+#include <cstdio>
+#include <cstdlib>
 #include "tcx_internal.h"
 #include "ptx.cuh"
 
@@ -84,7 +97,7 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64
   nt = r / gm;
 }
 
-template <int CG, int KIND, int NH>
+template <int CG, int KIND, int NH, int PM, int PN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
@@ -94,19 +107,38 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem* sm = (Smem*)(smem + C_::SMEM_DATA + C_::STG_BYTES);
 
+  constexpr int P = PM * PN;                 // CTA pairs per cluster
+  constexpr int CL = CG * P;                 // CTAs per cluster
+  static_assert(P == 1 || (CG == 2 && NH == 1), "multicast clusters: CTA pairs, 256-wide tile");
   const int warp = threadIdx.x / 32;
-  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const uint32_t crank = CG > 1 ? cluster_ctarank() : 0;
+  const bool mc = P > 1 && cluster_nctarank() == (uint32_t)CL;    // this group formed one cluster
+  const uint32_t rank = crank % CG;          // rank inside the CTA pair
+  const uint32_t pair = (blockIdx.x % CL) / CG;                   // pair slot inside the group
+  const int pm = (int)(pair % PM), pn = (int)(pair / PM);
+  const uint32_t lead_rank = mc ? pair * CG : 0;                  // this pair's leader CTA (cluster rank)
   const bool leader = rank == 0;
+  if (P > 1 && crank != (mc ? blockIdx.x % CL : blockIdx.x % CG)) __trap();   // cluster = aligned CTA block
 
   const int64_t m_tiles = (M + C_::TILE_M - 1) / C_::TILE_M;
   const int64_t n_tiles = (N + C_::TILE_N - 1) / C_::TILE_N;
-  const int64_t num_tiles = m_tiles * n_tiles;
+  const int64_t sm_tiles = (m_tiles + PM - 1) / PM;     // cluster tiles (PM x PN pair tiles each)
+  const int64_t sn_tiles = (n_tiles + PN - 1) / PN;
+  const int64_t num_tiles = sm_tiles * sn_tiles;
   const int64_t k_blocks = (K * KindT<KIND>::ESIZE + KBYTES - 1) / KBYTES;
-  const int64_t cluster_id = blockIdx.x / CG;
-  const int64_t num_clusters = gridDim.x / CG;
+  const int64_t cluster_id = blockIdx.x / CL;
+  const int64_t num_clusters = gridDim.x / CL;
+  // this pair's tile of cluster tile `tile` (a pair past the M / N edge computes on TMA zero fill
+  // and its stores are clipped: it still feeds its multicast slices to the other pairs)
+  auto pair_tile = [&](int64_t tile, int64_t& mt, int64_t& nt) {
+    int64_t smt, snt;
+    tile_coords(tile, sm_tiles, sn_tiles, group_m, smt, snt);
+    mt = smt * PM + pm;
+    nt = snt * PN + pn;
+  };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C_::STAGES; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], 1); }
+    for (int s = 0; s < C_::STAGES; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], mc ? P : 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&sm->tmem_full[a], 1); mbar_init(&sm->tmem_empty[a], EPI_WARPS * CG); }
     for (int w = 0; w < EPI_WARPS; ++w) { mbar_init(&sm->cbar[w][0], 1); mbar_init(&sm->cbar[w][1], 1); }
     fence_mbar_init();
@@ -114,7 +146,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   if (warp == 0 && elect_one()) { tma_prefetch(&tmA); tma_prefetch(&tmB); tma_prefetch(&tmC); tma_prefetch(&tmD); }
   if (warp == 2) { tmem_alloc<CG>(&sm->tmem_base, 512); tmem_relinquish<CG>(); }
   tc05_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if constexpr (CG > 1) cluster_sync(); else __syncthreads();
   tc05_fence_after();
   const uint32_t tmem_base = sm->tmem_base;
 
@@ -122,12 +154,16 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     // ================= TMA producer =================
     if (elect_one()) {
       int stage = 0; uint32_t phase = 0;
-      const uint32_t full0_cluster = CG == 2 ? mapa(smem_u32(&sm->full[0]), 0) : 0;
+      const uint32_t full0_cluster = CG == 2 ? mapa(smem_u32(&sm->full[0]), lead_rank) : 0;
+      constexpr int A_ROWS = BM / PN, B_ROWS = C_::BN_LOAD / PM;       // rows this CTA loads
+      uint16_t mask_a = 0, mask_b = 0;                                   // CTAs sharing them
+      for (int j = 0; j < PN; ++j) mask_a |= (uint16_t)(1u << ((pm + PM * j) * CG + rank));
+      for (int i = 0; i < PM; ++i) mask_b |= (uint16_t)(1u << ((i + PM * pn) * CG + rank));
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int64_t mt, nt;
-        tile_coords(tile, m_tiles, n_tiles, group_m, mt, nt);
-        const int arow = (int)(mt * C_::TILE_M + rank * BM);
-        const int brow = (int)(nt * C_::TILE_N + rank * C_::BN_LOAD);     // + h * BN for N-half h
+        pair_tile(tile, mt, nt);
+        const int arow = (int)(mt * C_::TILE_M + rank * BM);               // + j * A_ROWS for slice j
+        const int brow = (int)(nt * C_::TILE_N + rank * C_::BN_LOAD);      // + h * BN for N-half h
         for (int64_t kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&sm->empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C_::STAGE_BYTES;
@@ -140,9 +176,21 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           } else {
             if (leader) mbar_arrive_expect_tx(&sm->full[stage], 2 * C_::STAGE_BYTES);
             const uint32_t bar = full0_cluster + stage * 8;
-            tma_load_2d_cg2(sa, &tmA, bar, kx, arow);
+            if (PN > 1 && mc) {
+              tma_load_2d_cg2_mc(sa + pn * A_ROWS * KBYTES, &tmA, bar, kx, arow + pn * A_ROWS, mask_a);
+            } else {
 #pragma unroll
-            for (int h = 0; h < NH; ++h) tma_load_2d_cg2(sb + h * C_::HALF_BYTES, &tmB, bar, kx, brow + h * BN);
+              for (int j = 0; j < PN; ++j) tma_load_2d_cg2(sa + j * A_ROWS * KBYTES, &tmA, bar, kx, arow + j * A_ROWS);
+            }
+            if (PM > 1 && mc) {
+              tma_load_2d_cg2_mc(sb + pm * B_ROWS * KBYTES, &tmB, bar, kx, brow + pm * B_ROWS, mask_b);
+            } else {
+#pragma unroll
+              for (int h = 0; h < NH; ++h)
+#pragma unroll
+                for (int i = 0; i < PM; ++i)
+                  tma_load_2d_cg2(sb + h * C_::HALF_BYTES + i * B_ROWS * KBYTES, &tmB, bar, kx, brow + h * BN + i * B_ROWS);
+            }
           }
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -163,6 +211,14 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           umma<CG, KIND == KIND_F16ACC ? KIND_F16 : KIND>(tmem_d + h * BN, sdesc(sa + k * UMMA_KBYTES, 16, 1024, 2),
                                                           sdesc(sb + k * UMMA_KBYTES, 16, 1024, 2), idesc,
                                                           (acc16_c || (kb | k)) ? 1u : 0u);
+      };
+      // a slot's commit reaches every CTA that fed it (P > 1: the whole cluster); the accumulator's
+      // reaches both CTAs of this pair
+      auto commit_slot = [&](uint64_t* bar) {
+        if (P > 1 && mc) tc05_commit_mc(bar, (uint16_t)((1u << CL) - 1)); else tc05_commit<CG>(bar);
+      };
+      auto commit_acc = [&](uint64_t* bar) {
+        if (P > 1 && mc) tc05_commit_mc(bar, (uint16_t)(3u << lead_rank)); else tc05_commit<CG>(bar);
       };
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         const uint32_t tmem_d = tmem_base + acc * BN * NH;
@@ -208,8 +264,8 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           if (elect_one()) {
 #pragma unroll
             for (int h = 0; h < NH; ++h) issue(stage, h, kb, tmem_d);
-            tc05_commit<CG>(&sm->empty[stage]);                   // frees the smem slot
-            if (kb == k_blocks - 1) tc05_commit<CG>(&sm->tmem_full[acc]);   // accumulator ready
+            commit_slot(&sm->empty[stage]);                       // frees the smem slot
+            if (kb == k_blocks - 1) commit_acc(&sm->tmem_full[acc]);   // accumulator ready
           }
           __syncwarp();
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
@@ -228,13 +284,13 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     constexpr int CH = BN / 32;
     uint8_t* stg = smem + C_::SMEM_DATA + e * 8192;
     uint64_t* cbar = &sm->cbar[e][0];
-    uint32_t cph[2] = {0u, 0u};
-    const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), 0) : smem_u32(&sm->tmem_empty[0]);
+    uint32_t cph = 0u;                            // bit b: phase of cbar[b] (a register, not a local array)
+    const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), lead_rank) : smem_u32(&sm->tmem_empty[0]);
     const int64_t my_tiles = cluster_id < num_tiles ? (num_tiles - 1 - cluster_id) / num_clusters + 1 : 0;
     const uint32_t lane_off = (uint32_t)(e * 32) << 16;
     auto coords = [&](int64_t it, int ch, int& x, int& y) {
       int64_t mt, nt;
-      tile_coords(cluster_id + it * num_clusters, m_tiles, n_tiles, group_m, mt, nt);
+      pair_tile(cluster_id + it * num_clusters, mt, nt);
       y = (int)(mt * C_::TILE_M + rank * BM + e * 32);
       x = (int)(nt * C_::TILE_N + ch * 32);
     };
@@ -253,8 +309,8 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
 #pragma unroll 1
       for (int ch = 0; ch < CH; ++ch) {
         const int b = ch & 1;
-        mbar_wait(&cbar[b], cph[b]);
-        cph[b] ^= 1u;
+        mbar_wait(&cbar[b], (cph >> b) & 1u);
+        cph ^= 1u << b;
         const uint8_t* rowp = stg + b * 2048 + lane * 64;
         uint32_t r[32];
 #pragma unroll
@@ -322,14 +378,14 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     constexpr int CH = NH * BN / 32;              // 32-column chunks per tile (over both halves)
     uint8_t* stg = smem + C_::SMEM_DATA + e * 8192;
     uint64_t* cbar = &sm->cbar[e][0];
-    uint32_t cph[2] = {0u, 0u};
-    const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), 0) : smem_u32(&sm->tmem_empty[0]);
+    uint32_t cph = 0u;                            // bit b: phase of cbar[b] (a register, not a local array)
+    const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), lead_rank) : smem_u32(&sm->tmem_empty[0]);
     const int64_t my_tiles = cluster_id < num_tiles ? (num_tiles - 1 - cluster_id) / num_clusters + 1 : 0;
     const int64_t nq = my_tiles * CH;
     auto coords = [&](int64_t q, int& x, int& y) {
       const int64_t it = q / CH;
       int64_t mt, nt;
-      tile_coords(cluster_id + it * num_clusters, m_tiles, n_tiles, group_m, mt, nt);
+      pair_tile(cluster_id + it * num_clusters, mt, nt);
       y = (int)(mt * C_::TILE_M + rank * BM + e * 32);
       x = (int)(nt * C_::TILE_N + (q % CH) * 32);
     };
@@ -370,8 +426,8 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           tmem_ld_32x32b_x32(tmem_base + (acc * NH + hn) * BN + ((ch + 1) % (BN / 32)) * 32 + lane_off, vn);
         }
         if (has_c) {
-          mbar_wait(&cbar[b], cph[b]);
-          cph[b] ^= 1u;
+          mbar_wait(&cbar[b], (cph >> b) & 1u);
+          cph ^= 1u << b;
         } else if (q >= 2) {
           if (lane == 0) bulk_wait_read<1>();     // the store of chunk q-2 has read buffer b
           __syncwarp();
@@ -417,7 +473,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   }
 
   tc05_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if constexpr (CG > 1) cluster_sync(); else __syncthreads();
   if (warp == 2) { tc05_fence_after(); tmem_dealloc<CG>(tmem_base, 512); }
 }
 
@@ -431,16 +487,17 @@ __global__ void fill_c_kernel(const T* C, int64_t ldc, T* D, int64_t ldd, int64_
   }
 }
 
-template <int CG, int KIND, int NH>
+template <int CG, int KIND, int NH, int PM = 1, int PN = 1>
 tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUtensorMapDataType dt, int a_fmt) {
   using C_ = Cfg<CG, NH>;
   constexpr int ES = KindT<KIND>::ESIZE;
+  constexpr int CL = CG * PM * PN;
   CUtensorMap tA, tB;
   tcx_status st = make_tmap_2d(&tA, dt, a.A, (uint64_t)a.K, (uint64_t)a.M, (uint64_t)(a.lda * ES),
-                               KBYTES / ES, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+                               KBYTES / ES, BM / PN, CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != TCX_OK) return st;
   st = make_tmap_2d(&tB, dt, a.B, (uint64_t)a.K, (uint64_t)a.N, (uint64_t)(a.ldb * ES),
-                    KBYTES / ES, C_::BN_LOAD, CU_TENSOR_MAP_SWIZZLE_128B);
+                    KBYTES / ES, C_::BN_LOAD / PM, CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != TCX_OK) return st;
   // C and D: 32 x 32 boxes of 4-byte elements (128-byte rows) through 128B-swizzled staging
   // (FP16 accumulate: 32 x 32 boxes of FP16, 64-byte rows, 64B-swizzled)
@@ -457,23 +514,28 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
   } else {
     tC = tD;                                                  // unused (has_c = 0)
   }
-  auto kern = gemm_dense_kernel<CG, KIND, NH>;
+  auto kern = gemm_dense_kernel<CG, KIND, NH, PM, PN>;
   TCX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_TOTAL));
   const int64_t m_tiles = (a.M + C_::TILE_M - 1) / C_::TILE_M;
   const int64_t n_tiles = (a.N + C_::TILE_N - 1) / C_::TILE_N;
-  int64_t clusters = m_tiles * n_tiles;
-  int64_t max_clusters = dev.sm_count / CG;
-  if (a.max_ctas > 0 && a.max_ctas / CG < max_clusters) max_clusters = a.max_ctas / CG > 0 ? a.max_ctas / CG : 1;
-  if (clusters > max_clusters) clusters = max_clusters;
+  int64_t clusters = ((m_tiles + PM - 1) / PM) * ((n_tiles + PN - 1) / PN);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(clusters * CG));
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = C_::SMEM_TOTAL;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr; cfg.numAttrs = 1;
+  attr[1].id = cudaLaunchAttributePreferredClusterDimension;       // CL-CTA groups where a GPC has room
+  attr[1].val.preferredClusterDim.x = CL; attr[1].val.preferredClusterDim.y = 1; attr[1].val.preferredClusterDim.z = 1;
+  cfg.attrs = attr; cfg.numAttrs = CL > CG ? 2 : 1;
+  int64_t max_clusters = dev.sm_count / CL;                        // CTA groups (persistent)
+  if (a.max_ctas > 0 && a.max_ctas / CL < max_clusters) max_clusters = a.max_ctas / CL > 0 ? a.max_ctas / CL : 1;
+  if (clusters > max_clusters) clusters = max_clusters;
+  cfg.gridDim = dim3((unsigned)(clusters * CL));
+  if (getenv("TCX_DEBUG_LAUNCH"))
+    fprintf(stderr, "tcx_gemm: grid %u CTAs, cluster %d (pairs %dx%d), %lld cluster tiles\n", cfg.gridDim.x, CL, PM, PN,
+            (long long)(((m_tiles + PM - 1) / PM) * ((n_tiles + PN - 1) / PN)));
   const uint32_t idesc = make_idesc(KIND, a_fmt, BM * CG, BN);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
                                   a.C ? 1 : 0, idesc, a.group_m > 0 ? a.group_m : GROUP_M));
@@ -503,14 +565,22 @@ tcx_status launch_kind(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CU
   // higher clock under the power cap), but the single-buffered accumulator exposes the epilogue,
   // whose FP32 C read + D write bursts from all CTAs at once (profiles/r01_dense_tile_study.txt);
   // the double-buffered 256 x 256 tile is faster for this API's FP32 C/D.
-  const bool wide = a.tile_n == 512;
-  return wide ? launch_t<2, KIND, 2>(a, dev, s, dt, a_fmt) : launch_t<2, KIND, 1>(a, dev, s, dt, a_fmt);
+  if (a.tile_n == 512) return launch_t<2, KIND, 2>(a, dev, s, dt, a_fmt);
+  if (a.pairs_m == 2 && a.pairs_n == 2) return launch_t<2, KIND, 1, 2, 2>(a, dev, s, dt, a_fmt);
+  if (a.pairs_m == 2) return launch_t<2, KIND, 1, 2, 1>(a, dev, s, dt, a_fmt);
+  if (a.pairs_n == 2) return launch_t<2, KIND, 1, 1, 2>(a, dev, s, dt, a_fmt);
+  return launch_t<2, KIND, 1>(a, dev, s, dt, a_fmt);
 }
 
 tcx_status launch_gemm_dense(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
-  if (a.cd == TCX_F16)     // FP16 accumulate (F16 inputs only; validated by the front end)
-    return a.cta_group == 1 ? launch_t<1, KIND_F16ACC, 1>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 0)
-                            : launch_t<2, KIND_F16ACC, 1>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 0);
+  if (a.cd == TCX_F16) {   // FP16 accumulate (F16 inputs only; validated by the front end)
+    constexpr CUtensorMapDataType h = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    if (a.cta_group == 1) return launch_t<1, KIND_F16ACC, 1>(a, dev, s, h, 0);
+    if (a.pairs_m == 2 && a.pairs_n == 2) return launch_t<2, KIND_F16ACC, 1, 2, 2>(a, dev, s, h, 0);
+    if (a.pairs_m == 2) return launch_t<2, KIND_F16ACC, 1, 2, 1>(a, dev, s, h, 0);
+    if (a.pairs_n == 2) return launch_t<2, KIND_F16ACC, 1, 1, 2>(a, dev, s, h, 0);
+    return launch_t<2, KIND_F16ACC, 1>(a, dev, s, h, 0);
+  }
   switch (a.ab) {
     case TCX_F16: return launch_kind<KIND_F16>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 0);
     case TCX_BF16: return launch_kind<KIND_F16>(a, dev, s, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 1);

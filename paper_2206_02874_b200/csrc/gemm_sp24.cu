@@ -32,6 +32,11 @@ constexpr int GROUP_M = 8;            // default raster group (cluster-tile rows
 // into each SM, whose TMA ingress the 2:4 stream otherwise saturates.  Both halves'
 // accumulators fill TMEM (2 x 240 columns + the metadata ring), so the accumulator is
 // single-buffered: per-half empty barriers and a half-0 lookahead as in gemm_dense.cu's wide tile.
+// PM x PN > 1 (CTA pair, MW = 0): groups of PM x PN pairs launched as preferred clusters, as in
+// gemm_dense.cu.  In a formed cluster the pairs of a column share B — each loads one of the stage's
+// two 64-element K boxes of B and multicasts it — and the pairs of a row share sA (a 1/PN row
+// slice each); metadata atoms are per pair.  A group the hardware did not place as one cluster
+// runs as independent pairs on the same tiles.
 template <int CG, int KIND, int MW = 0>
 struct SpCfg {
   static constexpr int MH = MW ? 2 : 1;                    // M-halves per tile (accumulators)
@@ -83,7 +88,7 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64
   nt = r / gm;
 }
 
-template <int CG, int KIND, int MW>
+template <int CG, int KIND, int MW, int PM, int PN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmC,
@@ -96,18 +101,36 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem* sm = (Smem*)(smem + C_::SMEM_DATA + C_::STG_BYTES);
 
+  constexpr int P = PM * PN;                 // CTA pairs per group
+  constexpr int CL = CG * P;                 // CTAs per group
+  static_assert(P == 1 || (CG == 2 && !MW), "multicast groups: CTA pairs, 256-row tile");
+  static_assert(PM <= 2, "B is shared as its two K boxes");
   const int warp = threadIdx.x / 32;
-  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const uint32_t crank = CG > 1 ? cluster_ctarank() : 0;
+  const bool mc = P > 1 && cluster_nctarank() == (uint32_t)CL;    // this group formed one cluster
+  const uint32_t rank = crank % CG;
+  const uint32_t pair = (blockIdx.x % CL) / CG;
+  const int pm = (int)(pair % PM), pn = (int)(pair / PM);
+  const uint32_t lead_rank = mc ? pair * CG : 0;
   const bool leader = rank == 0;
+  if (P > 1 && crank != (mc ? blockIdx.x % CL : blockIdx.x % CG)) __trap();
   const int64_t m_tiles = M / C_::TILE_M;
   const int64_t n_tiles = (N + BN - 1) / BN;
-  const int64_t num_tiles = m_tiles * n_tiles;
+  const int64_t sm_tiles = (m_tiles + PM - 1) / PM;
+  const int64_t sn_tiles = (n_tiles + PN - 1) / PN;
+  const int64_t num_tiles = sm_tiles * sn_tiles;
   const int64_t k_blocks = K / KL;
-  const int64_t cluster_id = blockIdx.x / CG;
-  const int64_t num_clusters = gridDim.x / CG;
+  const int64_t cluster_id = blockIdx.x / CL;
+  const int64_t num_clusters = gridDim.x / CL;
+  auto pair_tile = [&](int64_t tile, int64_t& mt, int64_t& nt) {
+    int64_t smt, snt;
+    tile_coords(tile, sm_tiles, sn_tiles, group_m, smt, snt);
+    mt = smt * PM + pm;
+    nt = snt * PN + pn;
+  };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C_::STAGES; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], 1); }
+    for (int s = 0; s < C_::STAGES; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], mc ? P : 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&sm->tmem_full[a], 1); mbar_init(&sm->tmem_empty[a], EPI_WARPS * CG); }
     for (int w = 0; w < EPI_WARPS; ++w) { mbar_init(&sm->cbar[w][0], 1); mbar_init(&sm->cbar[w][1], 1); }
     fence_mbar_init();
@@ -122,10 +145,14 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (warp == 0) {
     if (elect_one()) {
       int stage = 0; uint32_t phase = 0;
-      const uint32_t full0_cluster = CG == 2 ? mapa(smem_u32(&sm->full[0]), 0) : 0;
+      const uint32_t full0_cluster = CG == 2 ? mapa(smem_u32(&sm->full[0]), lead_rank) : 0;
+      constexpr int A_ROWS = BM / PN;
+      uint16_t mask_a = 0, mask_b = 0;
+      for (int j = 0; j < PN; ++j) mask_a |= (uint16_t)(1u << ((pm + PM * j) * CG + rank));
+      for (int i = 0; i < PM; ++i) mask_b |= (uint16_t)(1u << ((i + PM * pn) * CG + rank));
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int64_t mt, nt;
-        tile_coords(tile, m_tiles, n_tiles, group_m, mt, nt);
+        pair_tile(tile, mt, nt);
         const int64_t mrow = mt * C_::TILE_M + rank * BM;            // + h * BM * CG for M-half h
         const int brow = (int)(nt * BN + rank * C_::BN_LOAD);
         for (int64_t kb = 0; kb < k_blocks; ++kb) {
@@ -148,11 +175,20 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
           for (int h = 0; h < MH; ++h) {
             const int64_t mrow_h = mrow + h * BM * CG;
-            load(sa + h * C_::A_HALF, &tmA, ka, (int)mrow_h);
+            if (PN > 1 && mc) {
+              tma_load_2d_cg2_mc(sa + h * C_::A_HALF + pn * A_ROWS * 128, &tmA, bar, ka, (int)mrow_h + pn * A_ROWS, mask_a);
+            } else {
+#pragma unroll
+              for (int j = 0; j < PN; ++j) load(sa + h * C_::A_HALF + j * A_ROWS * 128, &tmA, ka, (int)mrow_h + j * A_ROWS);
+            }
             load(se + h * 2048 * C_::META_ATOMS, &tmE, 0, (int)(((mrow_h / 128) * k_blocks + kb) * 16 * C_::META_ATOMS));
           }
-          load(sb, &tmB, kx, brow);
-          load(sb + C_::B_HALF, &tmB, kx + C_::BOX, brow);
+          if (PM > 1 && mc) {
+            tma_load_2d_cg2_mc(sb + pm * C_::B_HALF, &tmB, bar, kx + pm * C_::BOX, brow, mask_b);
+          } else {
+            load(sb, &tmB, kx, brow);
+            load(sb + C_::B_HALF, &tmB, kx + C_::BOX, brow);
+          }
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -182,6 +218,12 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             umma_sp<CG, KIND>(tmem_d, ad, bd, e & ~1u, idesc | (e & 1u), (kb | j) ? 1u : 0u);
           }
         }
+      };
+      auto commit_slot = [&](uint64_t* bar) {
+        if (P > 1 && mc) tc05_commit_mc(bar, (uint16_t)((1u << CL) - 1)); else tc05_commit<CG>(bar);
+      };
+      auto commit_acc = [&](uint64_t* bar) {
+        if (P > 1 && mc) tc05_commit_mc(bar, (uint16_t)(3u << lead_rank)); else tc05_commit<CG>(bar);
       };
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int64_t kb0 = 0;
@@ -223,8 +265,8 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           if (elect_one()) {
 #pragma unroll
             for (int h = 0; h < MH; ++h) issue(stage, h, kb, MW ? tmem_base + h * BN : tmem_d);
-            tc05_commit<CG>(&sm->empty[stage]);
-            if (kb == k_blocks - 1) tc05_commit<CG>(&sm->tmem_full[acc]);
+            commit_slot(&sm->empty[stage]);
+            if (kb == k_blocks - 1) commit_acc(&sm->tmem_full[acc]);
           }
           __syncwarp();
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
@@ -244,13 +286,13 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     constexpr int CH = HCH * MH;                 // chunks per tile
     uint8_t* stg = smem + C_::SMEM_DATA + e * 4096;
     uint64_t* cbar = &sm->cbar[e][0];
-    uint32_t cph[2] = {0u, 0u};
-    const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), 0) : smem_u32(&sm->tmem_empty[0]);
+    uint32_t cph = 0u;                            // bit b: phase of cbar[b] (a register, not a local array)
+    const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), lead_rank) : smem_u32(&sm->tmem_empty[0]);
     const int64_t my_tiles = cluster_id < num_tiles ? (num_tiles - 1 - cluster_id) / num_clusters + 1 : 0;
     const int64_t nq = my_tiles * CH;
     auto coords = [&](int64_t q, int& x, int& y) {
       int64_t mt, nt;
-      tile_coords(cluster_id + (q / CH) * num_clusters, m_tiles, n_tiles, group_m, mt, nt);
+      pair_tile(cluster_id + (q / CH) * num_clusters, mt, nt);
       const int ch = (int)(q % CH);
       y = (int)(mt * C_::TILE_M + (ch / HCH) * BM * CG + rank * BM + e * 32);
       x = (int)(nt * BN + (ch % HCH) * 16);
@@ -296,8 +338,8 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           if (lane == 0) mbar_arrive_cluster(tmem_empty_cluster + (MW ? ch / HCH : acc) * 8);
         }
         if (has_c) {
-          mbar_wait(&cbar[b], cph[b]);
-          cph[b] ^= 1u;
+          mbar_wait(&cbar[b], (cph >> b) & 1u);
+          cph ^= 1u << b;
         } else if (q >= 2) {
           if (lane == 0) bulk_wait_read<1>();     // the store of chunk q-2 has read buffer b
           __syncwarp();
@@ -341,15 +383,16 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (warp == 2) { tc05_fence_after(); tmem_dealloc<CG>(tmem_base, 512); }
 }
 
-template <int CG, int KIND, int MW = 0>
+template <int CG, int KIND, int MW = 0, int PM = 1, int PN = 1>
 tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
+  constexpr int CL = CG * PM * PN;
   using C_ = SpCfg<CG, KIND, MW>;
   if (a.M % C_::TILE_M) return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: M %% %d != 0", C_::TILE_M);
   const CUtensorMapDataType dt = KIND == KIND_I8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                  : KIND == KIND_TF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                  : a.ab == TCX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tA, tB, tE;
-  tcx_status st = make_tmap_2d(&tA, dt, a.A, (uint64_t)(a.K / 2), (uint64_t)a.M, (uint64_t)(a.lda * C_::ES), C_::BOX, BM,
+  tcx_status st = make_tmap_2d(&tA, dt, a.A, (uint64_t)(a.K / 2), (uint64_t)a.M, (uint64_t)(a.lda * C_::ES), C_::BOX, BM / PN,
                                CU_TENSOR_MAP_SWIZZLE_128B);
   if (st != TCX_OK) return st;
   st = make_tmap_2d(&tB, dt, a.B, (uint64_t)a.K, (uint64_t)a.N, (uint64_t)(a.ldb * C_::ES), C_::BOX, C_::BN_LOAD,
@@ -371,22 +414,24 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   } else {
     tC = tD;
   }
-  auto kern = gemm_sp24_kernel<CG, KIND, MW>;
+  auto kern = gemm_sp24_kernel<CG, KIND, MW, PM, PN>;
   TCX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_TOTAL));
-  const int64_t tiles = (a.M / C_::TILE_M) * ((a.N + BN - 1) / BN);
-  int64_t clusters = tiles;
-  int64_t max_clusters = dev.sm_count / CG;
-  if (a.max_ctas > 0 && a.max_ctas / CG < max_clusters) max_clusters = a.max_ctas / CG > 0 ? a.max_ctas / CG : 1;
+  const int64_t m_tiles = a.M / C_::TILE_M, n_tiles = (a.N + BN - 1) / BN;
+  int64_t clusters = ((m_tiles + PM - 1) / PM) * ((n_tiles + PN - 1) / PN);
+  int64_t max_clusters = dev.sm_count / CL;
+  if (a.max_ctas > 0 && a.max_ctas / CL < max_clusters) max_clusters = a.max_ctas / CL > 0 ? a.max_ctas / CL : 1;
   if (clusters > max_clusters) clusters = max_clusters;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(clusters * CG));
+  cfg.gridDim = dim3((unsigned)(clusters * CL));
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = C_::SMEM_TOTAL;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr; cfg.numAttrs = 1;
+  attr[1].id = cudaLaunchAttributePreferredClusterDimension;
+  attr[1].val.preferredClusterDim.x = CL; attr[1].val.preferredClusterDim.y = 1; attr[1].val.preferredClusterDim.z = 1;
+  cfg.attrs = attr; cfg.numAttrs = CL > CG ? 2 : 1;
   // idesc: sparse flag [2], c format [4,6) (F32 = 1, S32 = 2), a/b format [7,10)/[10,13)
   // (f16 0, bf16 1; s8 signed 1), N>>3 [17,23), M>>4 [24,29); saturate [3] = 0 (wrap)
   const uint32_t fmt = KIND == KIND_TF32 ? 2u : (KIND == KIND_I8 || a.ab == TCX_BF16) ? 1u : 0u;
@@ -399,17 +444,24 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   return TCX_OK;
 }
 
+template <int KIND>
+tcx_status launch_sp_kind(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
+  if (a.cta_group == 1) return launch_sp<1, KIND>(a, dev, s);
+  // tile_m = 512 (opts.tile_n field reused as the sparse tile height): the M-wide pair tile
+  if constexpr (KIND != KIND_I8)
+    if (a.tile_n == 512 && a.M % 512 == 0) return launch_sp<2, KIND, 1>(a, dev, s);
+  if (a.pairs_m == 2 && a.pairs_n == 2) return launch_sp<2, KIND, 0, 2, 2>(a, dev, s);
+  if (a.pairs_m == 2) return launch_sp<2, KIND, 0, 2, 1>(a, dev, s);
+  if (a.pairs_n == 2) return launch_sp<2, KIND, 0, 1, 2>(a, dev, s);
+  return launch_sp<2, KIND>(a, dev, s);
+}
+
 }  // namespace
 
 tcx_status launch_gemm_sp24(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
-  if (a.ab == TCX_S8) return a.cta_group == 1 ? launch_sp<1, KIND_I8>(a, dev, s) : launch_sp<2, KIND_I8>(a, dev, s);
-  // tile_m = 512 (opts.tile_n field reused as the sparse tile height): the M-wide pair tile
-  const bool mw = a.tile_n == 512 && a.cta_group != 1 && a.M % 512 == 0;
-  if (a.ab == TCX_TF32)
-    return a.cta_group == 1 ? launch_sp<1, KIND_TF32>(a, dev, s)
-                            : (mw ? launch_sp<2, KIND_TF32, 1>(a, dev, s) : launch_sp<2, KIND_TF32>(a, dev, s));
-  return a.cta_group == 1 ? launch_sp<1, KIND_F16>(a, dev, s)
-                          : (mw ? launch_sp<2, KIND_F16, 1>(a, dev, s) : launch_sp<2, KIND_F16>(a, dev, s));
+  if (a.ab == TCX_S8) return launch_sp_kind<KIND_I8>(a, dev, s);
+  if (a.ab == TCX_TF32) return launch_sp_kind<KIND_TF32>(a, dev, s);
+  return launch_sp_kind<KIND_F16>(a, dev, s);
 }
 
 }  // namespace tcx

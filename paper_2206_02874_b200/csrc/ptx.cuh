@@ -32,6 +32,9 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); return r;
 }
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r; asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r)); return r;
+}
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -122,6 +125,17 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* m,
       :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(x), "r"(y)
       : "memory");
 }
+// the same, multicast: the box lands at this smem offset in every CTA of `mask`; each destination's
+// complete_tx goes to the barrier at the same offset in the CTA of the destination's pair that
+// `bar_cluster` names (the pair leader)
+__device__ __forceinline__ void tma_load_2d_cg2_mc(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int x, int y,
+                                                   uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;"
+      :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(x), "r"(y), "h"(mask)
+      : "memory");
+}
 // L2 prefetch of a 2D tile (no smem, no barrier): warms L2 so a later load of the same box hits
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int x, int y) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
@@ -175,6 +189,11 @@ __device__ __forceinline__ void tc05_commit(uint64_t* bar) {
   else
     asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
                  :: "r"(smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
+}
+// CTA-pair commit arriving on the barrier at this offset in every CTA of `mask`
+__device__ __forceinline__ void tc05_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               :: "r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 
 // ------------------------------------------------------------------ UMMA descriptors

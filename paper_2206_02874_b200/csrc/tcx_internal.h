@@ -54,6 +54,8 @@ struct GemmArgs {
   int max_ctas;
   int group_m;    // 0 = default
   int tile_n;     // dense: 256 / 512 / 0 = auto
+  int pairs_m = 1;  // dense, CTA pair: multicast cluster shape in pairs
+  int pairs_n = 1;
 };
 tcx_status launch_gemm_dense(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);
 tcx_status launch_gemm_sp24(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);

@@ -81,8 +81,23 @@ __device__ __forceinline__ void load16(Frag16& f, const uint16_t* A, const uint1
 // at once and waits (griddepcontrol.wait) for the previous grid's completion and memory flush
 // before its first load, so stream semantics are unchanged while back-to-back launches of this
 // latency-bound kernel overlap their launch/ramp (C1: 3.15 -> 2.52 us per call, profiles/).
-__device__ __forceinline__ void pdl_prologue() {
+// Between the two, each warp L2-prefetches the operands of its first tile (lane 0, bulk prefetch of
+// the tile's contiguous A, B and C bytes): a prefetch returns nothing to the SM and L2 is where
+// every SM's writes land, so a line the previous grid writes afterwards is updated in place and the
+// loads after the wait still see it — stream order is kept, while this launch's DRAM reads overlap
+// the tail of the previous grid instead of starting after it.
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
+struct TileBytes { uint32_t a, b, c; };   // contiguous bytes of one tile's A_t, B_t, C_t
+__device__ __forceinline__ void pdl_prologue(const void* A, const void* B, const void* C, TileBytes tb,
+                                             int64_t first_tile, int64_t count) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if ((threadIdx.x & 31) == 0 && first_tile < count) {
+    l2_prefetch((const uint8_t*)A + first_tile * tb.a, tb.a);
+    l2_prefetch((const uint8_t*)B + first_tile * tb.b, tb.b);
+    if (C) l2_prefetch((const uint8_t*)C + first_tile * tb.c, tb.c);
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
@@ -92,7 +107,7 @@ __global__ void __launch_bounds__(WARPS * 32) tiles16_kernel(const uint16_t* __r
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  pdl_prologue();
+  pdl_prologue(A, B, C, TileBytes{512, 256, 512}, warp, count);
   int64_t tile = warp;
   if (tile >= count) return;
   Frag16 cur;
@@ -123,7 +138,7 @@ __global__ void __launch_bounds__(WARPS * 32) tiles16x_kernel(const uint32_t* __
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   constexpr int W = KT / 2;          // 32-bit words per row of A_t / B_t
-  pdl_prologue();
+  pdl_prologue(A, B, C, TileBytes{16u * W * 4, 8u * W * 4, H ? 256u : 512u}, warp, count);
   for (int64_t tile = warp; tile < count; tile += nwarps) {
     const uint32_t* At = A + tile * 16 * W;
     const uint32_t* Bt = B + tile * 8 * W;
@@ -167,7 +182,7 @@ __global__ void __launch_bounds__(WARPS * 32) tiles_tf32_kernel(const uint32_t* 
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  pdl_prologue();
+  pdl_prologue(A, B, C, TileBytes{16u * KT * 4, 8u * KT * 4, 512u}, warp, count);
   for (int64_t tile = warp; tile < count; tile += nwarps) {
     const uint32_t* At = A + tile * 16 * KT;
     const uint32_t* Bt = B + tile * 8 * KT;
@@ -200,7 +215,7 @@ __global__ void __launch_bounds__(WARPS * 32) tiles_s8_kernel(const int8_t* __re
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  pdl_prologue();
+  pdl_prologue(A, B, C, TileBytes{512, 256, 512}, warp, count);
   for (int64_t tile = warp; tile < count; tile += nwarps) {
     const uint32_t* A32 = (const uint32_t*)(A + tile * 512);   // row r, k quad j -> A32[r*8 + j]
     const uint32_t* B32 = (const uint32_t*)(B + tile * 256);

@@ -205,3 +205,63 @@ def test_gemm_bad_tile_n_rejected():
     A, B, C = _problem(256, 256, 64, "bf16", seed=1)
     with pytest.raises(tcx.TcxError):
         tcx.gemm(A, B, C, tile_n=384)
+
+
+MC_SHAPES = [(256, 256, 128), (512, 512, 512), (200, 600, 72), (264, 520, 40), (768, 1280, 1024), (1, 4, 8),
+             (1300, 260, 192)]
+
+
+@pytest.mark.parametrize("pairs", [(1, 2), (2, 1), (2, 2)])
+@pytest.mark.parametrize("fmt", ["bf16", "tf32", "s8"])
+@pytest.mark.parametrize("shape", MC_SHAPES)
+def test_gemm_multicast_cluster_whole_matrix(fmt, shape, pairs):
+    """TMA-multicast clusters of CTA pairs (tcx_gemm_opts.pairs_m/pairs_n): ragged M/N/K, shapes whose
+    pair-tile count is odd (a pair past the edge computes on zero fill and feeds the others)."""
+    M, N, K = shape
+    if fmt == "s8":
+        K = max(16, (K + 15) // 16 * 16)
+    A, B, C = _problem(M, N, K, fmt, seed=M + 5 * N + K)
+    D = tcx.gemm(A, B, C, tf32=(fmt == "tf32"), pairs=pairs)
+    torch.cuda.synchronize()
+    _full_check(fmt, A, B, C, D)
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "s8", "f16acc"])
+def test_gemm_multicast_equals_default_and_persistent(fmt):
+    """a multicast cluster changes who loads which operand rows, not the MMA sequence: D is bit-
+    identical to the default pair kernel's, also with few clusters looping over many tiles."""
+    M, N, K = 1536, 2304, 1024
+    if fmt == "f16acc":
+        A, B, _ = _problem(M, N, K, "f16", seed=23, with_c=False)
+        C = tcxgen.normal_matrix((M, N), "f16", 23, tcxgen.STREAM_C, DEV)
+        kw = dict(f16_acc=True)
+        view = torch.int16
+    else:
+        A, B, C = _problem(M, N, K, fmt, seed=23)
+        kw = {}
+        view = torch.int32
+    ref = tcx.gemm(A, B, C, **kw)
+    for pairs in [(1, 2), (2, 1), (2, 2)]:
+        for max_ctas in (0, 8, 16):
+            D = tcx.gemm(A, B, C, pairs=pairs, max_ctas=max_ctas, **kw)
+            torch.cuda.synchronize()
+            assert torch.equal(ref.view(view), D.view(view)), (pairs, max_ctas)
+
+
+def test_gemm_multicast_config3_full_size():
+    """BASELINE configs[2] through the 2 x 2 multicast cluster: sampled oracle parity + full-coverage bound."""
+    M = N = K = 8192
+    A, B, _ = _problem(M, N, K, "bf16", seed=0, with_c=False)
+    C = torch.zeros(M, N, dtype=torch.float32, device=DEV)
+    D = tcx.gemm(A, B, C, pairs=(2, 2))
+    torch.cuda.synchronize()
+    rows, cols = gemm_sample_coords(M, N, 256, 256, nsamp=65536)
+    check_gemm_samples(O.BF16, A, B, C, D, rows, cols, K, "C3 mc22")
+    _float64_full_coverage(A, B, C, D, K)
+
+
+def test_gemm_bad_pairs_rejected():
+    A, B, C = _problem(256, 256, 64, "bf16", seed=1)
+    for kw in (dict(pairs=(3, 1)), dict(pairs=(2, 1), cta_group=1), dict(pairs=(1, 2), tile_n=512)):
+        with pytest.raises(tcx.TcxError):
+            tcx.gemm(A, B, C, **kw)

@@ -208,3 +208,36 @@ def test_sparse_m_wide_integer_bit_exact_bf16():
     ref = dense.double() @ B.double().T + C.double()
     torch.cuda.synchronize()
     assert torch.equal(D.double(), ref)
+
+
+@pytest.mark.parametrize("pairs", [(2, 1), (1, 2), (2, 2)])
+@pytest.mark.parametrize("shape", [(256, 240, 128), (768, 496, 640), (1280, 1008, 256)])
+def test_sparse_multicast_groups_vs_oracle_and_default(shape, pairs):
+    """groups of CTA pairs sharing B (pairs_m) / sA (pairs_n) by TMA multicast: vs the oracle on
+    every output (odd pair-tile counts: a pair past the edge computes on zero fill), bit-identical to
+    the default pair kernel, also with few groups looping over many tiles."""
+    M, N, K = shape
+    vals, meta, _ = _dense_24(M, K, M + 11 * N + K)
+    B = tcxgen.normal_matrix((N, K), "f16", M + N, tcxgen.STREAM_B, DEV)
+    C = tcxgen.normal_matrix((M, N), "f32", M + N, tcxgen.STREAM_C, DEV)
+    hw = tcx.sp24_pack_meta(meta, M, K)
+    Dm = tcx.gemm_sp24(vals, hw, B, C, pairs=pairs)
+    Dn = tcx.gemm_sp24(vals, hw, B, C)
+    Dp = tcx.gemm_sp24(vals, hw, B, C, pairs=pairs, max_ctas=8)
+    torch.cuda.synchronize()
+    assert torch.equal(Dm.view(torch.int32), Dn.view(torch.int32))
+    assert torch.equal(Dm.view(torch.int32), Dp.view(torch.int32))
+    ii, jj = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+    ref, absv = O.gemm_samples(O.F16, O.sp24_expand(host_bits(vals), host_bits(meta), K), host_bits(B),
+                               host_bits(C), ii.ravel(), jj.ravel())
+    fp_bound_check(host_bits(Dm).ravel(), ref, absv, K, f"sp24 mc {shape} {pairs}")
+
+
+def test_sparse_multicast_bad_options_rejected():
+    M, N, K = 256, 240, 128
+    vals, meta, _ = _dense_24(M, K, 3)
+    B = tcxgen.normal_matrix((N, K), "f16", 3, tcxgen.STREAM_B, DEV)
+    hw = tcx.sp24_pack_meta(meta, M, K)
+    for kw in (dict(pairs=(3, 1)), dict(pairs=(2, 1), cta_group=1), dict(pairs=(2, 1), tile_m=512)):
+        with pytest.raises(tcx.TcxError):
+            tcx.gemm_sp24(vals, hw, B, None, **kw)

@@ -119,3 +119,17 @@ def _sparse_i8_nodense(M, K, seed):
     v = tcxgen.int32_matrix((M, K // 2), seed, tcxgen.STREAM_SPVAL, -128, 126, DEV)
     v = torch.where(v >= 0, v + 1, v)
     return v.to(torch.int8), meta, None
+
+
+@pytest.mark.parametrize("pairs", [(2, 1), (1, 2), (2, 2)])
+def test_i8_sparse_multicast_groups_bit_exact(pairs):
+    M, N, K = 768, 1008, 768
+    vals, meta, dense = _sparse_i8(M, K, 41)
+    B = tcxgen.int8_matrix((N, K), 41, tcxgen.STREAM_B, DEV)
+    C = tcxgen.int32_matrix((M, N), 41, tcxgen.STREAM_C, device=DEV)
+    hw = tcx.sp24_pack_meta(meta, M, K, ab=tcx.S8)
+    D = tcx.gemm_sp24(vals, hw, B, C, pairs=pairs)
+    torch.cuda.synchronize()
+    ii, jj = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+    ref, _ = O.gemm_samples(O.S8, host_bits(dense), host_bits(B), host_bits(C), ii.ravel(), jj.ravel())
+    assert np.array_equal(host_bits(D).ravel(), ref)

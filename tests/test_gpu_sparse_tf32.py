@@ -125,3 +125,16 @@ def test_tf32_sparse_m_wide_bit_exact():
     ref = dense.double() @ B.double().T
     torch.cuda.synchronize()
     assert torch.equal(D.double(), ref)
+
+
+@pytest.mark.parametrize("pairs", [(2, 1), (2, 2)])
+def test_tf32_sparse_multicast_bit_exact(pairs):
+    M, N, K = 768, 720, 512
+    dense = _sparse12(M, K, 13, integer=True)
+    vals, meta = tcx.sp24_compress(dense, tf32=True)
+    B = tcxgen.int32_matrix((N, K), 13, 2, -8, 8, DEV).to(torch.float32)
+    hw = tcx.sp24_pack_meta(meta, M, K, ab=tcx.TF32)
+    D = tcx.gemm_sp24(vals, hw, B, None, tf32=True, pairs=pairs)
+    ref = dense.double() @ B.double().T
+    torch.cuda.synchronize()
+    assert torch.equal(D.double(), ref)

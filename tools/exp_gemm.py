@@ -2,7 +2,8 @@
 """Kernel-configuration sweep for the GEMM paths (raster group, CTA mode).
 
 usage: python tools/exp_gemm.py c5|c3|c4|c3tf32 [steps] [variant ...]
-variant = "g<group_m>c<cta_group>[w]" e.g. g8c2, g16c2, g8c1, g8c2w (w = the 512-wide tile).  Prints one JSON line per variant
+variant = "g<group_m>c<cta_group>[w][p<pm><pn>]" e.g. g8c2, g16c2, g8c1, g8c2w (w = the 512-wide tile),
+g8c2p12 (multicast cluster of 1 x 2 CTA pairs).  Prints one JSON line per variant
 with device time (CUDA events), TFLOP/s, NVML SM clock / power during the run, and whether D is
 bit-identical to the first variant's D (the knobs change no arithmetic)."""
 import json
@@ -20,10 +21,12 @@ import bench  # noqa: E402
 
 
 def parse(v):
-    m = re.fullmatch(r"g(\d+)c(\d)(w?)", v)
+    m = re.fullmatch(r"g(\d+)c(\d)(w?)(?:p(\d)(\d))?", v)
     kw = dict(group_m=int(m.group(1)), cta_group=int(m.group(2)))
     if m.group(3):
         kw["wide"] = True
+    if m.group(4):
+        kw["pairs"] = (int(m.group(4)), int(m.group(5)))
     return kw
 
 

@@ -15,7 +15,10 @@ fns = {"cublas": lambda: torch.matmul(w.A, w.B.t(), out=D16),
        "narrow_noC": lambda: w.tcx.gemm(w.A, w.B, None, w.D, tile_n=256),
        "wide_noC": lambda: w.tcx.gemm(w.A, w.B, None, w.D, tile_n=512),
        "narrow": lambda: w.tcx.gemm(w.A, w.B, w.C, w.D, tile_n=256),
-       "wide": lambda: w.tcx.gemm(w.A, w.B, w.C, w.D, tile_n=512)}
+       "wide": lambda: w.tcx.gemm(w.A, w.B, w.C, w.D, tile_n=512),
+       "mc12": lambda: w.tcx.gemm(w.A, w.B, w.C, w.D, pairs=(1, 2)),
+       "mc21": lambda: w.tcx.gemm(w.A, w.B, w.C, w.D, pairs=(2, 1)),
+       "mc22": lambda: w.tcx.gemm(w.A, w.B, w.C, w.D, pairs=(2, 2))}
 for _ in range(reps):
     fns[v]()
 torch.cuda.synchronize()
