@@ -149,6 +149,10 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   if constexpr (CG > 1) cluster_sync(); else __syncthreads();
   tc05_fence_after();
   const uint32_t tmem_base = sm->tmem_base;
+  // PDL: the setup above (barriers, TMEM allocation, descriptor prefetch) overlapped the previous
+  // grid's tail; no global memory is touched before its completion
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     // ================= TMA producer =================
@@ -523,12 +527,14 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = C_::SMEM_TOTAL;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributePreferredClusterDimension;       // CL-CTA groups where a GPC has room
-  attr[1].val.preferredClusterDim.x = CL; attr[1].val.preferredClusterDim.y = 1; attr[1].val.preferredClusterDim.z = 1;
-  cfg.attrs = attr; cfg.numAttrs = CL > CG ? 2 : 1;
+  cudaLaunchAttribute attr[3];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CG; attr[1].val.clusterDim.y = 1; attr[1].val.clusterDim.z = 1;
+  attr[2].id = cudaLaunchAttributePreferredClusterDimension;       // CL-CTA groups where a GPC has room
+  attr[2].val.preferredClusterDim.x = CL; attr[2].val.preferredClusterDim.y = 1; attr[2].val.preferredClusterDim.z = 1;
+  cfg.attrs = attr; cfg.numAttrs = CL > CG ? 3 : 2;
   int64_t max_clusters = dev.sm_count / CL;                        // CTA groups (persistent)
   if (a.max_ctas > 0 && a.max_ctas / CL < max_clusters) max_clusters = a.max_ctas / CL > 0 ? a.max_ctas / CL : 1;
   if (clusters > max_clusters) clusters = max_clusters;

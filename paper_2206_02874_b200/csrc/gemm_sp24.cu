@@ -16,6 +16,7 @@
 // 128 B of sA per row), B two 32-element boxes, one metadata atom; layout as kind::f16 over 2K.
 // "The hardware selector determines which values should participate ... on the fly":
 // the MMA skips the zero products; throughput doubles at the same latency.
+#include <cstdlib>
 #include "tcx_internal.h"
 #include "ptx.cuh"
 
@@ -141,6 +142,10 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc05_fence_after();
   const uint32_t tmem_base = sm->tmem_base;
+  // PDL: the setup above (barriers, TMEM allocation, descriptor prefetch) overlapped the previous
+  // grid's tail; no global memory is touched before its completion
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -426,12 +431,14 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = C_::SMEM_TOTAL;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributePreferredClusterDimension;
-  attr[1].val.preferredClusterDim.x = CL; attr[1].val.preferredClusterDim.y = 1; attr[1].val.preferredClusterDim.z = 1;
-  cfg.attrs = attr; cfg.numAttrs = CL > CG ? 2 : 1;
+  cudaLaunchAttribute attr[3];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;     // PDL (see pdl_wait in the kernel)
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CG; attr[1].val.clusterDim.y = 1; attr[1].val.clusterDim.z = 1;
+  attr[2].id = cudaLaunchAttributePreferredClusterDimension;
+  attr[2].val.preferredClusterDim.x = CL; attr[2].val.preferredClusterDim.y = 1; attr[2].val.preferredClusterDim.z = 1;
+  cfg.attrs = attr; cfg.numAttrs = CL > CG ? 3 : 2;
   // idesc: sparse flag [2], c format [4,6) (F32 = 1, S32 = 2), a/b format [7,10)/[10,13)
   // (f16 0, bf16 1; s8 signed 1), N>>3 [17,23), M>>4 [24,29); saturate [3] = 0 (wrap)
   const uint32_t fmt = KIND == KIND_TF32 ? 2u : (KIND == KIND_I8 || a.ab == TCX_BF16) ? 1u : 0u;
