@@ -171,7 +171,8 @@ def mma_chain(A0, Bs, tf32=False, Ds=None):
 
 
 # ---------------------------------------------------------------------------------------- GEMM
-def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, tile_n=0, f16_acc=False, pairs=(0, 0)):
+def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, tile_n=0, f16_acc=False, pairs=(0, 0),
+         _fault=0):
     """Dense D = A x B + C with A (M, K), B stored (N, K) ("row.col"), C/D (M, N).
     f16_acc: FP16 inputs with an FP16 accumulator (C, D float16; C is the MMA's C operand).
     pairs = (pairs_m, pairs_n): TMA-multicast cluster of CTA pairs (tcx_gemm_opts)."""
@@ -184,7 +185,7 @@ def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, t
         raise ValueError("f16_acc: C must be float16")
     if D is None:
         D = torch.empty((M, N), dtype={S32: torch.int32, F16: torch.float16, F32: torch.float32}[cd], device=A.device)
-    opts = GemmOpts(cta_group, max_ctas, group_m, tile_n, pairs[0], pairs[1])
+    opts = GemmOpts(cta_group, max_ctas, group_m, tile_n, pairs[0], pairs[1], (ctypes.c_int * 2)(_fault, 0))
     _check(lib().tcx_gemm_ex(ab, cd, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
                              _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
                              ctypes.byref(opts), _stream(A)))

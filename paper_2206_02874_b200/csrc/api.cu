@@ -218,6 +218,9 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
       return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: multicast clusters need cta_group 2 and the 256-wide tile");
     g.pairs_m = pm;
     g.pairs_n = pn;
+#if TCX_WATCHDOG
+    g.fault = opts->reserved[0];   // fault injection exists only in the debug library
+#endif
   }
   if (K == 0) return launch_fill_c(g, (cudaStream_t)stream);
   return launch_gemm_dense(g, dev, (cudaStream_t)stream);

@@ -101,7 +101,7 @@ template <int CG, int KIND, int NH, int PM, int PN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
-                  int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc, int group_m) {
+                  int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc, int group_m, int fault) {
   using C_ = Cfg<CG, NH>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -180,6 +180,16 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           } else {
             if (leader) mbar_arrive_expect_tx(&sm->full[stage], 2 * C_::STAGE_BYTES);
             const uint32_t bar = full0_cluster + stage * 8;
+#if TCX_WATCHDOG
+            // fault injection (debug library): the first A load is never issued, its barrier never
+            // completes, and the MMA warp's bounded wait traps
+            if (fault == 1 && tile == cluster_id && kb == 0) {
+              if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
+              continue;
+            }
+#else
+            (void)fault;
+#endif
             if (PN > 1 && mc) {
               tma_load_2d_cg2_mc(sa + pn * A_ROWS * KBYTES, &tmA, bar, kx, arow + pn * A_ROWS, mask_a);
             } else {
@@ -544,7 +554,7 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
             (long long)(((m_tiles + PM - 1) / PM) * ((n_tiles + PN - 1) / PN)));
   const uint32_t idesc = make_idesc(KIND, a_fmt, BM * CG, BN);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
-                                  a.C ? 1 : 0, idesc, a.group_m > 0 ? a.group_m : GROUP_M));
+                                  a.C ? 1 : 0, idesc, a.group_m > 0 ? a.group_m : GROUP_M, a.fault));
   count_launch();
   return TCX_OK;
 }

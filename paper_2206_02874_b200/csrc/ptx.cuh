@@ -79,20 +79,36 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t pa
       : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
   return ok != 0;
 }
+// Debug builds (libtcx_debug.so, -DTCX_WATCHDOG=1) bound every barrier wait: a phase that does not
+// complete within TCX_WATCHDOG_NS of wall time (globaltimer) traps, so a pipeline bug becomes a
+// launch error returned through the C-ABI instead of a hung GPU.
+#ifndef TCX_WATCHDOG_NS
+#define TCX_WATCHDOG_NS 4000000000ull
+#endif
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t a = smem_u32(bar);
 #if TCX_WATCHDOG
-  long long t0 = clock64();
+  const uint64_t t0 = globaltimer_ns();
 #endif
   while (!mbar_try_wait(a, parity)) {
 #if TCX_WATCHDOG
-    if (clock64() - t0 > (1ll << 34)) __trap();
+    if (globaltimer_ns() - t0 > TCX_WATCHDOG_NS) __trap();
 #endif
   }
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t a = smem_u32(bar);
-  while (!mbar_try_wait_cluster(a, parity)) {}
+#if TCX_WATCHDOG
+  const uint64_t t0 = globaltimer_ns();
+#endif
+  while (!mbar_try_wait_cluster(a, parity)) {
+#if TCX_WATCHDOG
+    if (globaltimer_ns() - t0 > TCX_WATCHDOG_NS) __trap();
+#endif
+  }
 }
 
 // ------------------------------------------------------------------ fences

@@ -56,6 +56,7 @@ struct GemmArgs {
   int tile_n;     // dense: 256 / 512 / 0 = auto
   int pairs_m = 1;  // dense, CTA pair: multicast cluster shape in pairs
   int pairs_n = 1;
+  int fault = 0;    // debug builds only (TCX_WATCHDOG): 1 = the dense producer drops one TMA load
 };
 tcx_status launch_gemm_dense(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);
 tcx_status launch_gemm_sp24(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);

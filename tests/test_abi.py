@@ -34,6 +34,16 @@ def test_library_exports_every_declared_symbol():
     assert set(tcx.EXPORTS) <= exported
 
 
+def test_debug_library_exports_the_same_boundary():
+    """libtcx_debug.so (watchdog-bounded waits) is the same ABI; built here like the product."""
+    from paper_2206_02874_b200 import build
+    path = build.build(debug=True)
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (tcx_\w+)", out))
+    assert set(_declared()) <= exported
+    assert path != tcx.LIB_PATH
+
+
 def test_host_only_calls_without_gpu():
     L = tcx.lib()
     assert L.tcx_status_string(2) == b"TCX_ERR_UNSUPPORTED"

@@ -1,0 +1,104 @@
+"""The debug library (libtcx_debug.so: every mbarrier wait bounded by a globaltimer watchdog, plus
+a fault-injection hook) — SURVEY §5 "race detection / failure detection": a pipeline bug must end
+as an error returned to the caller, never as a hung GPU.  Each case runs in a subprocess with
+TCX_LIB_PATH naming the debug build (a trapped kernel poisons its CUDA context)."""
+import os
+import subprocess
+import sys
+import textwrap
+
+import numpy as np
+import pytest
+import torch
+
+import tcxgen
+import paper_2206_02874_b200 as tcx
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DEBUG_LIB = os.path.join(ROOT, "paper_2206_02874_b200", "libtcx_debug.so")
+
+
+def _run(code, tmp_path, timeout=120):
+    if not os.path.exists(DEBUG_LIB):
+        from paper_2206_02874_b200 import build as b
+        b.build(debug=True)
+    env = dict(os.environ, TCX_LIB_PATH=DEBUG_LIB, PYTHONPATH=ROOT)
+    script = tmp_path / "case.py"
+    script.write_text(textwrap.dedent(code))
+    return subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=timeout,
+                          cwd=str(tmp_path))
+
+
+PROBLEM = """
+import numpy as np, torch
+import tcxgen, paper_2206_02874_b200 as tcx
+assert tcx.LIB_PATH.endswith("libtcx_debug.so"), tcx.LIB_PATH
+dev = "cuda"
+A = tcxgen.normal_matrix((512, 320), "bf16", 5, tcxgen.STREAM_A, dev)
+B = tcxgen.normal_matrix((768, 320), "bf16", 5, tcxgen.STREAM_B, dev)
+C = tcxgen.normal_matrix((512, 768), "f32", 5, tcxgen.STREAM_C, dev)
+"""
+
+
+def test_debug_library_matches_product(tmp_path):
+    """the watchdog changes no arithmetic: dense (default and multicast groups), sparse and tile
+    results from the debug build are bit-identical to the product build's."""
+    code = PROBLEM + """
+vals, meta = tcxgen.sp24_problem(512, 256, 6, "f16", dev)
+Bs = tcxgen.normal_matrix((480, 256), "f16", 6, tcxgen.STREAM_B, dev)
+hw = tcx.sp24_pack_meta(meta, 512, 256)
+At = tcxgen.uniform_matrix((64, 16, 16), "f16", 0, 1, device=dev)
+Bt = tcxgen.uniform_matrix((64, 8, 16), "f16", 0, 2, device=dev)
+out = {"d": tcx.gemm(A, B, C), "d22": tcx.gemm(A, B, C, pairs=(2, 2)), "s": tcx.gemm_sp24(vals, hw, Bs, None),
+       "t": tcx.mma_tiles(At, Bt, None)}
+torch.cuda.synchronize()
+np.savez("out.npz", **{k: v.cpu().view(torch.int32).numpy() for k, v in out.items()})
+print("OK")
+"""
+    r = _run(code, tmp_path)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-2000:]
+    got = np.load(tmp_path / "out.npz")
+    dev = "cuda"
+    A = tcxgen.normal_matrix((512, 320), "bf16", 5, tcxgen.STREAM_A, dev)
+    B = tcxgen.normal_matrix((768, 320), "bf16", 5, tcxgen.STREAM_B, dev)
+    C = tcxgen.normal_matrix((512, 768), "f32", 5, tcxgen.STREAM_C, dev)
+    vals, meta = tcxgen.sp24_problem(512, 256, 6, "f16", dev)
+    Bs = tcxgen.normal_matrix((480, 256), "f16", 6, tcxgen.STREAM_B, dev)
+    hw = tcx.sp24_pack_meta(meta, 512, 256)
+    At = tcxgen.uniform_matrix((64, 16, 16), "f16", 0, 1, device=dev)
+    Bt = tcxgen.uniform_matrix((64, 8, 16), "f16", 0, 2, device=dev)
+    ref = {"d": tcx.gemm(A, B, C), "d22": tcx.gemm(A, B, C), "s": tcx.gemm_sp24(vals, hw, Bs, None),
+           "t": tcx.mma_tiles(At, Bt, None)}
+    torch.cuda.synchronize()
+    for k, v in ref.items():
+        assert np.array_equal(got[k], v.cpu().view(torch.int32).numpy()), k
+
+
+def test_watchdog_turns_a_stalled_pipeline_into_an_error(tmp_path):
+    """fault injection: the producer drops one TMA load, so a full barrier never completes; the
+    MMA warp's bounded wait traps and the caller gets a CUDA error (not a hang)."""
+    code = PROBLEM + """
+import time
+t0 = time.time()
+try:
+    D = tcx.gemm(A, B, C, _fault=1)
+    torch.cuda.synchronize()
+    print("NO_ERROR")
+except Exception as e:
+    print("TRAPPED", round(time.time() - t0, 1), type(e).__name__, str(e).splitlines()[0][:200])
+"""
+    r = _run(code, tmp_path, timeout=90)
+    assert "TRAPPED" in r.stdout, (r.stdout[-1000:], r.stderr[-2000:])
+    secs = float(r.stdout.split("TRAPPED")[1].split()[0])
+    assert secs < 60
+
+
+def test_product_library_ignores_the_fault_hook():
+    """the product build has no fault injection: reserved[0] = 1 computes normally."""
+    A = tcxgen.normal_matrix((256, 128), "bf16", 1, tcxgen.STREAM_A, "cuda")
+    B = tcxgen.normal_matrix((256, 128), "bf16", 1, tcxgen.STREAM_B, "cuda")
+    D1 = tcx.gemm(A, B, None, _fault=1)
+    D0 = tcx.gemm(A, B, None)
+    torch.cuda.synchronize()
+    assert torch.equal(D0, D1)
