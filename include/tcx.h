@@ -95,7 +95,8 @@ tcx_status tcx_gemm(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
 typedef struct {
   int cta_group;   /* 1 or 2 (CTA pair, tcgen05 cta_group::2) */
   int max_ctas;    /* cap on persistent CTAs (0 = all SMs) */
-  int group_m;     /* tile raster: cluster-tile rows that sweep N together (0 = default) */
+  int group_m;     /* tile raster (0 = default): > 0, that many cluster-tile rows sweep N together;
+                      < 0, |group_m| cluster-tile columns sweep M together */
   int tile_n;      /* 0 = library choice; 512: tcx_gemm's 256 x 512 pair tile (two N = 256 MMAs
                       share A), tcx_gemm_sp24's 512 x 240 pair tile (two M-halves share B;
                       F16/BF16/TF32, M % 512 == 0) */

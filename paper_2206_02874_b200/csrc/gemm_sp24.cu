@@ -78,15 +78,22 @@ struct Smem {
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64_t n_tiles, int group_m,
+__device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64_t n_tiles, int group,
                                             int64_t& mt, int64_t& nt) {
-  int64_t per_group = (int64_t)group_m * n_tiles;
-  int64_t g = tile / per_group;
-  int64_t first_m = g * group_m;
-  int64_t gm = m_tiles - first_m < group_m ? m_tiles - first_m : group_m;
-  int64_t r = tile - g * per_group;
-  mt = first_m + r % gm;
-  nt = r / gm;
+  // grouped raster.  group > 0: `group` m-tiles x all n-tiles per group, m fastest inside a group
+  // (the group's A rows stay in L2 while B streams past); group < 0: |group| n-tiles x all m-tiles,
+  // n fastest (B's columns stay while A streams) — the cheaper one re-reads the smaller operand
+  const bool by_m = group > 0;
+  const int64_t g_tiles = by_m ? group : -group;
+  const int64_t major = by_m ? m_tiles : n_tiles, minor = by_m ? n_tiles : m_tiles;
+  const int64_t per_group = g_tiles * minor;
+  const int64_t g = tile / per_group;
+  const int64_t first = g * g_tiles;
+  const int64_t gm = major - first < g_tiles ? major - first : g_tiles;
+  const int64_t r = tile - g * per_group;
+  const int64_t a = first + r % gm, b = r / gm;
+  mt = by_m ? a : b;
+  nt = by_m ? b : a;
 }
 
 template <int CG, int KIND, int MW, int PM, int PN>
@@ -446,7 +453,7 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   const uint32_t idesc = (1u << 2) | (cfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
                          ((uint32_t)((BM * CG) >> 4) << 24);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tE, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
-                                  a.C ? 1 : 0, idesc, a.group_m > 0 ? a.group_m : GROUP_M));
+                                  a.C ? 1 : 0, idesc, a.group_m != 0 ? a.group_m : GROUP_M));
   count_launch();
   return TCX_OK;
 }

@@ -265,3 +265,17 @@ def test_gemm_bad_pairs_rejected():
     for kw in (dict(pairs=(3, 1)), dict(pairs=(2, 1), cta_group=1), dict(pairs=(1, 2), tile_n=512)):
         with pytest.raises(tcx.TcxError):
             tcx.gemm(A, B, C, **kw)
+
+
+@pytest.mark.parametrize("group_m", [-1, -3, -8, 5])
+def test_gemm_raster_orders_bit_identical(group_m):
+    """the raster (group_m > 0: M-groups sweeping N; < 0: N-groups sweeping M) only reorders tiles:
+    D is bit-identical to the default, also with a persistent grid of few CTAs."""
+    M, N, K = 1300, 1800, 320
+    A, B, C = _problem(M, N, K, "bf16", seed=29)
+    ref = tcx.gemm(A, B, C)
+    D = tcx.gemm(A, B, C, group_m=group_m)
+    Dp = tcx.gemm(A, B, C, group_m=group_m, max_ctas=6)
+    torch.cuda.synchronize()
+    assert torch.equal(ref.view(torch.int32), D.view(torch.int32))
+    assert torch.equal(ref.view(torch.int32), Dp.view(torch.int32))

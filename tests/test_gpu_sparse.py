@@ -241,3 +241,18 @@ def test_sparse_multicast_bad_options_rejected():
     for kw in (dict(pairs=(3, 1)), dict(pairs=(2, 1), cta_group=1), dict(pairs=(2, 1), tile_m=512)):
         with pytest.raises(tcx.TcxError):
             tcx.gemm_sp24(vals, hw, B, None, **kw)
+
+
+@pytest.mark.parametrize("group_m", [-2, -8, 3])
+def test_sparse_raster_orders_bit_identical(group_m):
+    M, N, K = 1280, 1200, 256
+    vals, meta, _ = _dense_24(M, K, 33)
+    B = tcxgen.normal_matrix((N, K), "f16", 33, tcxgen.STREAM_B, DEV)
+    C = tcxgen.normal_matrix((M, N), "f32", 33, tcxgen.STREAM_C, DEV)
+    hw = tcx.sp24_pack_meta(meta, M, K)
+    ref = tcx.gemm_sp24(vals, hw, B, C)
+    D = tcx.gemm_sp24(vals, hw, B, C, group_m=group_m)
+    Dp = tcx.gemm_sp24(vals, hw, B, C, group_m=group_m, max_ctas=6)
+    torch.cuda.synchronize()
+    assert torch.equal(ref.view(torch.int32), D.view(torch.int32))
+    assert torch.equal(ref.view(torch.int32), Dp.view(torch.int32))

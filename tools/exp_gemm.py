@@ -21,7 +21,7 @@ import bench  # noqa: E402
 
 
 def parse(v):
-    m = re.fullmatch(r"g(\d+)c(\d)(w?)(?:p(\d)(\d))?", v)
+    m = re.fullmatch(r"g(-?\d+)c(\d)(w?)(?:p(\d)(\d))?", v)
     kw = dict(group_m=int(m.group(1)), cta_group=int(m.group(2)))
     if m.group(3):
         kw["wide"] = True
