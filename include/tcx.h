@@ -108,6 +108,14 @@ typedef struct {
                    /* to the default.                                                               */
   int reserved[2];
 } tcx_gemm_opts;
+/* Debug library only (libtcx_debug.so; the product returns TCX_ERR_UNSUPPORTED): per-tile timeline
+ * of later tcx_gemm / tcx_gemm_ex launches (CTA-pair kernel).  d_buf: device buffer of
+ * 4 * capacity uint64 (caller-owned, NULL = off); tile record i (cluster tile i of the launch's raster):
+ *   [0] = pair id << 32 | tile index, [1] = %globaltimer ns when the tile's first MMA issued,
+ *   [2] = when its last MMA was committed, [3] = when the epilogue issued its last store.
+ * Records past `capacity` are dropped.  Used to study L2 reuse across concurrent tiles. */
+tcx_status tcx_debug_trace(void* d_buf, int64_t capacity);
+
 tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
                        const void* A, int64_t lda, const void* B, int64_t ldb,
                        const void* C, int64_t ldc, void* D, int64_t ldd,

@@ -33,7 +33,7 @@ _STATUS = {0: "TCX_OK", 1: "TCX_ERR_INVALID_VALUE", 2: "TCX_ERR_UNSUPPORTED", 3:
 EXPORTS = ["tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_mma_chain", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
            "tcx_sp24_meta_hw_bytes", "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_gemm_sp24_ex", "tcx_round_tf32",
            "tcx_probe", "tcx_ldmatrix_dump",
-           "tcx_status_string", "tcx_last_error", "tcx_version", "tcx_launch_count"]
+           "tcx_status_string", "tcx_last_error", "tcx_version", "tcx_launch_count", "tcx_debug_trace"]
 
 
 class TcxError(RuntimeError):
@@ -91,8 +91,10 @@ def lib():
     L.tcx_last_error.restype = ctypes.c_char_p
     L.tcx_version.restype = ctypes.c_char_p
     L.tcx_launch_count.restype = ctypes.c_uint64
+    L.tcx_debug_trace.argtypes = [vp, i64]
     for f in ("tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_mma_chain", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
-              "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_gemm_sp24_ex", "tcx_round_tf32", "tcx_probe", "tcx_ldmatrix_dump"):
+              "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_gemm_sp24_ex", "tcx_round_tf32", "tcx_probe", "tcx_ldmatrix_dump",
+              "tcx_debug_trace"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -190,6 +192,16 @@ def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, t
                              _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
                              ctypes.byref(opts), _stream(A)))
     return D
+
+
+def debug_trace(buf=None):
+    """debug library only: record a per-tile timeline of later tcx_gemm launches into `buf`
+    (int64 CUDA tensor of 4 * capacity; None = off).  See include/tcx.h tcx_debug_trace."""
+    if buf is None:
+        _check(lib().tcx_debug_trace(None, 0))
+    else:
+        _dev_check(buf)
+        _check(lib().tcx_debug_trace(_ptr(buf), buf.numel() // 4))
 
 
 # ---------------------------------------------------------------------------------------- sparse

@@ -112,6 +112,11 @@ static tcx_status check_gemm_common(const char* fn, tcx_dtype ab, tcx_dtype cd, 
 
 using namespace tcx;
 
+#if TCX_WATCHDOG
+static uint64_t* g_trace = nullptr;   // tcx_debug_trace (debug library only)
+static int64_t g_trace_cap = 0;
+#endif
+
 extern "C" {
 
 const char* tcx_status_string(tcx_status s) {
@@ -130,6 +135,19 @@ const char* tcx_status_string(tcx_status s) {
 
 const char* tcx_last_error(void) { return t_err; }
 const char* tcx_version(void) { return "tcx 0.1 (sm_100a)"; }
+
+tcx_status tcx_debug_trace(void* d_buf, int64_t capacity) {
+#if TCX_WATCHDOG
+  if (capacity < 0 || (d_buf && ((uintptr_t)d_buf & 7)))
+    return set_error(TCX_ERR_INVALID_VALUE, "tcx_debug_trace: bad buffer / capacity");
+  g_trace = (uint64_t*)d_buf;
+  g_trace_cap = d_buf ? capacity : 0;
+  return TCX_OK;
+#else
+  (void)d_buf; (void)capacity;
+  return set_error(TCX_ERR_UNSUPPORTED, "tcx_debug_trace: only in the debug library (libtcx_debug.so)");
+#endif
+}
 uint64_t tcx_launch_count(void) { return g_launches.load(); }
 
 tcx_status tcx_mma_tiles(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, int64_t count, const void* A, const void* B,
@@ -222,6 +240,10 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
     g.fault = opts->reserved[0];   // fault injection exists only in the debug library
 #endif
   }
+#if TCX_WATCHDOG
+  g.trace = g_trace;
+  g.trace_cap = g_trace_cap;
+#endif
   if (K == 0) return launch_fill_c(g, (cudaStream_t)stream);
   return launch_gemm_dense(g, dev, (cudaStream_t)stream);
 }

@@ -107,7 +107,8 @@ template <int CG, int KIND, int NH, int PM, int PN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
-                  int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc, int group_m, int fault) {
+                  int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc, int group_m, int fault,
+                  uint64_t* trace, int64_t trace_cap) {
   using C_ = Cfg<CG, NH>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -194,7 +195,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
               continue;
             }
 #else
-            (void)fault;
+            (void)fault; (void)trace; (void)trace_cap;
 #endif
             if (PN > 1 && mc) {
               tma_load_2d_cg2_mc(sa + pn * A_ROWS * KBYTES, &tmA, bar, kx, arow + pn * A_ROWS, mask_a);
@@ -286,6 +287,15 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
             for (int h = 0; h < NH; ++h) issue(stage, h, kb, tmem_d);
             commit_slot(&sm->empty[stage]);                       // frees the smem slot
             if (kb == k_blocks - 1) commit_acc(&sm->tmem_full[acc]);   // accumulator ready
+#if TCX_WATCHDOG
+            if (trace && tile < trace_cap) {                      // debug tile timeline
+              if (kb == kb0) {
+                trace[4 * tile] = ((uint64_t)(cluster_id * P + pair) << 32) | (uint64_t)tile;
+                trace[4 * tile + 1] = globaltimer_ns();
+              }
+              if (kb == k_blocks - 1) trace[4 * tile + 2] = globaltimer_ns();
+            }
+#endif
           }
           __syncwarp();
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
@@ -487,6 +497,12 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         }
         load_c(q + 2);                                        // ... for the C chunk two ahead
       }
+#if TCX_WATCHDOG
+      if (trace && e == 0 && lane == 0 && rank == 0) {
+        const int64_t tile = cluster_id + it * num_clusters;
+        if (tile < trace_cap) trace[4 * tile + 3] = globaltimer_ns();
+      }
+#endif
       if (++acc == C_::NBUF) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) bulk_wait<0>();                            // stores complete before exit
@@ -560,7 +576,8 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
             (long long)(((m_tiles + PM - 1) / PM) * ((n_tiles + PN - 1) / PN)));
   const uint32_t idesc = make_idesc(KIND, a_fmt, BM * CG, BN);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
-                                  a.C ? 1 : 0, idesc, a.group_m != 0 ? a.group_m : GROUP_M, a.fault));
+                                  a.C ? 1 : 0, idesc, a.group_m != 0 ? a.group_m : GROUP_M, a.fault, a.trace,
+                                  a.trace_cap));
   count_launch();
   return TCX_OK;
 }

@@ -57,6 +57,8 @@ struct GemmArgs {
   int pairs_m = 1;  // dense, CTA pair: multicast cluster shape in pairs
   int pairs_n = 1;
   int fault = 0;    // debug builds only (TCX_WATCHDOG): 1 = the dense producer drops one TMA load
+  uint64_t* trace = nullptr;   // debug builds only: tile timeline (tcx_debug_trace)
+  int64_t trace_cap = 0;
 };
 tcx_status launch_gemm_dense(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);
 tcx_status launch_gemm_sp24(const GemmArgs& a, const DevInfo& dev, cudaStream_t s);

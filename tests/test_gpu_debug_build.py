@@ -102,3 +102,33 @@ def test_product_library_ignores_the_fault_hook():
     D0 = tcx.gemm(A, B, None)
     torch.cuda.synchronize()
     assert torch.equal(D0, D1)
+
+
+def test_tile_trace_records_every_tile(tmp_path):
+    """tcx_debug_trace: one record per cluster tile, start <= MMA end <= epilogue end, each pair's
+    tiles in raster order; the product library refuses the call."""
+    code = PROBLEM + """
+M, N, K = 1024, 1536, 512
+A = tcxgen.normal_matrix((M, K), "bf16", 8, tcxgen.STREAM_A, dev)
+B = tcxgen.normal_matrix((N, K), "bf16", 8, tcxgen.STREAM_B, dev)
+T = (M // 256) * (N // 256)
+buf = torch.zeros(4 * T, dtype=torch.int64, device=dev)
+tcx.debug_trace(buf)
+D = tcx.gemm(A, B, None, max_ctas=8)
+torch.cuda.synchronize()
+tcx.debug_trace(None)
+np.save("trace.npy", buf.view(T, 4).cpu().numpy())
+print("OK")
+"""
+    r = _run(code, tmp_path)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-2000:]
+    t = np.load(tmp_path / "trace.npy").astype(np.int64)
+    assert np.array_equal(t[:, 0] & 0xFFFFFFFF, np.arange(len(t)))
+    assert np.all(t[:, 1] > 0) and np.all(t[:, 1] <= t[:, 2]) and np.all(t[:, 2] <= t[:, 3])
+    pair = t[:, 0] >> 32
+    assert set(pair.tolist()) == set(range(4))                    # max_ctas = 8: four pairs
+    for p in range(4):
+        s = t[pair == p, 1]
+        assert np.all(np.diff(s) > 0)                             # a pair's tiles run in order
+    with pytest.raises(tcx.TcxError):
+        tcx.debug_trace(torch.zeros(8, dtype=torch.int64, device="cuda"))
