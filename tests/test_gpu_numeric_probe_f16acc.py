@@ -9,6 +9,7 @@ every tile is classified bit-exactly against
     truncation window and every block rounding at FP16's 11-bit significand);
   * two-stage models: an FP32-accumulator model (incl. the one observed for FP16 -> FP32,
     DESIGN.md §7) followed by one conversion FP32 -> FP16 (RNE or RZ);
+  * single-rounding models M16w32: the FP32 datapath's truncation window, one rounding into FP16;
 so "computation in high precision, converted only at the end" (PAPER.md:982) is tested, not assumed.
 Gate: every output of every tile within the FP16 bar of the oracle (tests/parity.py).
 Report: numeric_probe_f16acc_report.json in $TCX_REPORT_DIR (default gpurun_out/)."""
@@ -51,6 +52,12 @@ def models():
     return ms
 
 
+# aligned like the FP32 datapath (window p bits below FP32's significand), rounded ONCE into FP16:
+# the single-rounding alternative to the two-stage models (oracle.model_batch win_fmt = FP32)
+FP32_WINDOW = [(f"M16w32(g=16,p={p},{'RZ' if rz else 'RNE'},tz,{'c_after' if ca else 'c_in'},{('lead', 'esum', 'esum2')[em]})",
+                dict(g=16, p=p, rz=rz, c_after=ca, emode=em))
+               for em in (0, 2) for p in range(0, 9) for rz in (True, False) for ca in (False, True)]
+
 TWO_STAGE = [("exact32_RNE", dict(g=16, p=-1, rz=False, emode=0))] + [
     (f"M32(g=16,p={p},{'RZ' if rz else 'RNE'},tz,{'c_after' if ca else 'c_in'},esum2)",
      dict(g=16, p=p, rz=rz, c_after=ca, emode=2))
@@ -75,6 +82,8 @@ def test_numeric_probe_fp16_accumulate():
     gv = got_all[:, 0, 0]
     outs = {nm: O.model_batch(O.F16, a_rows, b_rows, c16, Ki=16, acc_fmt=O.F16, **kw) for nm, kw in models()}
     assert np.array_equal(outs["exact_RNE16"], ref[:, 0, 0])       # the model family's special case
+    for nm, kw in FP32_WINDOW:
+        outs[nm] = O.model_batch(O.F16, a_rows, b_rows, c16, Ki=16, acc_fmt=O.F16, win_fmt=O.F32, **kw)
     for nm, kw in TWO_STAGE:
         m32 = O.model_batch(O.F16, a_rows, b_rows, c32, Ki=16, **kw)
         outs[nm + "->RNE16"] = _f32_to_f16_bits(m32, False)

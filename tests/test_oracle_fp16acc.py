@@ -167,3 +167,43 @@ def test_gemm_samples_fp16_cd_integer_exact():
                             cd=O.F16)
     ref = (A.astype(np.float64) @ B.astype(np.float64).T + C.astype(np.float64)).astype(np.float16)
     assert np.array_equal(out.astype(np.uint16).reshape(M, N), ref.view(np.uint16))
+
+
+def _model16(a_vals, b_vals, c, p, rz, win):
+    a = _f16(a_vals)[None, :]
+    b = _f16(b_vals)[None, :]
+    cb = np.array([int(_f16([c])[0])], np.uint32)
+    out = O.model_batch(O.F16, a, b, cb, Ki=len(a_vals), g=len(a_vals), p=p, rz=rz, emode=2, acc_fmt=O.F16,
+                        win_fmt=win)
+    return float(np.array([out[0]], np.uint16).view(np.float16)[0])
+
+
+def test_fp32_window_single_rounding_closed_form():
+    """M16 with the FP32 truncation window (win_fmt = FP32): c = 1, products 2^-11 and 2^-25.
+    Exact sum 1 + 2^-11 + 2^-25 lies above FP16's tie at 1 + 2^-11 -> RNE up to 1 + 2^-10.
+      * window p = 3 (bits down to 2^(1-23-3) = 2^-25, c's esum2 frame is 2^1) keeps 2^-25 -> one
+        RNE into FP16 rounds up (the single-rounding model);
+      * p = 2 drops 2^-25 -> an exact tie -> even -> 1.0;
+      * the two-stage reading (FP32 RZ first) would land on the tie as well: 1.0 — which is what
+        separates the two readings."""
+    a, b = [2.0 ** -5, 2.0 ** -12], [2.0 ** -6, 2.0 ** -13]      # products 2^-11, 2^-25 exact in FP16 inputs
+    assert _model16(a, b, 1.0, p=3, rz=False, win=O.F32) == 1.0 + 2 ** -10
+    assert _model16(a, b, 1.0, p=2, rz=False, win=O.F32) == 1.0
+    assert _model16(a, b, 1.0, p=3, rz=True, win=O.F32) == 1.0
+    # the FP16-window family at p = 3 truncates at 2^(1-10-3) = 2^-12: both small products' bits
+    # below it vanish (2^-11 survives) -> tie -> 1.0
+    assert _model16(a, b, 1.0, p=3, rz=False, win=O.F16) == 1.0
+
+
+def test_fp32_window_wide_p_is_exact_rne16():
+    """with a window wider than any product/c spread (p = 60) nothing is truncated: the model is one
+    RNE of the exact sum into FP16 — the pinned exact oracle (dot_fp)."""
+    rng = np.random.default_rng(5)
+    n, K = 400, 16
+    A = np.stack([_rand_f16(rng, K, -8, 4) for _ in range(n)])
+    B = np.stack([_rand_f16(rng, K, -8, 4) for _ in range(n)])
+    C = np.array([_rand_f16(rng, 1, -6, 6)[0] for _ in range(n)], np.uint32)
+    got = O.model_batch(O.F16, A, B, C, Ki=16, g=16, p=60, rz=False, emode=2, acc_fmt=O.F16, win_fmt=O.F32)
+    for i in range(n):
+        want, _ = O.dot_fp(O.F16, A[i], B[i], int(C[i]), c_fmt=O.F16, out_fmt=O.F16)
+        assert got[i] == want, i
