@@ -2,8 +2,9 @@
 two chained k8), eight crafted classes, run through the paper's own instruction
 (mma.sync, tcx_mma_tiles) and through tcgen05 with C preloaded in tensor memory
 (tcx_mma_tiles_tc05).  Each probed element is classified bit-exactly against the model family
-M(g, p, R, t, o) (oracle/models.c), so B200's rounding / truncation / extra precision is reported
-as OBSERVED (north_star), plus the paper's mean-error tables for the three
+M(g, p, R, t, o, e) (oracle/models.c; e = esum2f reads a subnormal accumulator's exponent from its
+field, like the inputs'), so B200's rounding / truncation / extra precision is reported as OBSERVED
+(north_star), plus the paper's mean-error tables for the three
 probes (multiplication, inner-product add, accumulation add).
 
 Gate: every element within the FP bound of the exact oracle.  Report: JSON written to
@@ -27,14 +28,14 @@ FMTS = {"f16": (O.F16, 16), "bf16": (O.BF16, 16), "tf32": (O.TF32, 8)}
 
 def model_list(Ki):
     ms = [("exact_RNE", dict(g=Ki, p=-1, rz=False)), ("exact_RZ", dict(g=Ki, p=-1, rz=True))]
-    for em in (0, 1, 2):
-        for g in sorted({Ki, 8, 4, 2, 1}, reverse=True):
+    for em in (0, 1, 2, 3):
+        for g in (sorted({Ki, 8, 4, 2, 1}, reverse=True) if em < 3 else sorted({Ki, 8}, reverse=True)):
             for p in range(0, 9):
                 for rz in (True, False):
                     for fl in (False, True):
                         for ca in (False, True):
                             nm = (f"M(g={g},p={p},{'RZ' if rz else 'RNE'},{'floor' if fl else 'tz'},"
-                                  f"{'c_after' if ca else 'c_in'},{('lead', 'esum', 'esum2')[em]})")
+                                  f"{'c_after' if ca else 'c_in'},{('lead', 'esum', 'esum2', 'esum2f')[em]})")
                             ms.append((nm, dict(g=g, p=p, rz=rz, floor_mode=fl, c_after=ca, emode=em)))
     ms.append(("SEQ32_RNE(g=1,p=inf)", dict(g=1, p=-1, rz=False)))
     return ms

@@ -207,3 +207,52 @@ def test_seq32_matches_numpy_binary32():
         for x, y in zip(a, b):
             acc = np.float32(acc + np.float32(x * y))
         assert O.seq32(a, b, float(c), c_last=True) == float(np.float32(acc + c))
+
+
+def _bf16_bits(x):
+    return O.quantize(float(x), O.BF16)
+
+
+def _emode_out(emode, a_vals, b_vals, c_val, p=3, Ki=16):
+    a = np.array([_bf16_bits(x) for x in a_vals] + [0] * (Ki - len(a_vals)), np.uint16)[None, :]
+    b = np.array([_bf16_bits(x) for x in b_vals] + [0] * (Ki - len(b_vals)), np.uint16)[None, :]
+    cb = np.array([np.array([c_val], np.float32).view(np.uint32)[0]], np.uint32)
+    out = O.model_batch(O.BF16, a, b, cb, Ki=Ki, g=Ki, p=p, rz=True, emode=emode)
+    return float(f32_from_bits(out[0]))
+
+
+def test_field_exponent_accumulator_closed_form():
+    """emode 3 (the accumulator's exponent read from its exponent field): c = 2^-140 is an FP32
+    subnormal, so its field exponent is emin = -126 (frame -125) while its leading bit is -140
+    (frame -139).  Products: 2^-131 (a = 2^-65, b = 2^-66; nominal -130) and eight of 2^-152
+    (2^-76 x 2^-76; nominal -151), whose sum 2^-149 is one FP32 subnormal ulp.
+      * emode 2: e_max = -130 -> window 2^(-130-26) = 2^-156 keeps the 2^-152 products:
+        2^-131 + 2^-140 + 2^-149 (RZ is exact on the 2^-149 grid);
+      * emode 3: e_max = -125 (c) -> window 2^-151 truncates each 2^-152 product to 0:
+        2^-131 + 2^-140."""
+    a = [2.0 ** -65] + [2.0 ** -76] * 8
+    b = [2.0 ** -66] + [2.0 ** -76] * 8
+    c = 2.0 ** -140
+    assert _emode_out(2, a, b, c) == 2.0 ** -131 + 2.0 ** -140 + 2.0 ** -149
+    assert _emode_out(3, a, b, c) == 2.0 ** -131 + 2.0 ** -140
+    # with a normal c the two readings coincide (field exponent == leading bit)
+    assert _emode_out(3, a, b, 2.0 ** -120) == _emode_out(2, a, b, 2.0 ** -120)
+
+
+@pytest.mark.parametrize("fmt,Ki", [(O.F16, 16), (O.BF16, 16), (O.TF32, 8)])
+def test_field_exponent_equals_esum2_for_normal_c(fmt, Ki):
+    """emode 3 differs from the pinned emode 2 only through a subnormal accumulator: identical on
+    random tiles whose c (and every intermediate accumulator) is normal or zero."""
+    rng = np.random.default_rng(31 + fmt)
+    NPd = np.uint32 if fmt == O.TF32 else np.uint16
+    n, K = 500, 2 * Ki
+    A = np.array([[O.quantize(v, fmt) for v in rng.standard_normal(K) * 2.0 ** rng.integers(-6, 6, K)]
+                  for _ in range(n)], NPd)
+    B = np.array([[O.quantize(v, fmt) for v in rng.standard_normal(K) * 2.0 ** rng.integers(-6, 6, K)]
+                  for _ in range(n)], NPd)
+    C = (rng.standard_normal(n) * 2.0 ** rng.integers(-10, 10, n)).astype(np.float32).view(np.uint32)
+    C[::7] = 0
+    for p in (2, 3, 5):
+        m2 = O.model_batch(fmt, A, B, C, Ki=Ki, g=Ki, p=p, rz=True, emode=2)
+        m3 = O.model_batch(fmt, A, B, C, Ki=Ki, g=Ki, p=p, rz=True, emode=3)
+        assert np.array_equal(m2, m3), p
