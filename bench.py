@@ -51,6 +51,11 @@ def peaks():
 # nominal dense ratios vs bf16 (B200_PROFILING.md nominal table: tf32 1.1 vs 2.25; int8 = fp8 rate 4.5;
 # 2:4 sparse doubles the dense rate): peak for kind = measured bf16 peak x ratio
 KIND_RATIO = {"bf16": 1.0, "f16": 1.0, "f16acc": 1.0, "tf32": 0.5, "s8": 2.0, "sp16": 2.0, "sp8": 4.0, "sptf32": 1.0}
+# SURVEY §8(d)'s two extra denominators: the datasheet dense BF16 peak (2.25 PFLOP/s) x the same
+# ratio, and the clock-normalised peak 148 SMs x 4096 dense BF16 FMA/clk/SM x ratio x 2 x the SM clock
+# NVML saw during the timed region
+DATASHEET_BF16_TFLOPS = 2250.0
+BF16_FMA_PER_CLK_SM = 4096
 
 
 class ClockSampler:
@@ -422,6 +427,14 @@ def roofline(work, ms, pk, clocks=None):
         # figure is the matching denominator; `frac` stays against the burst peak
         ps = pk["bf16_sustained"] * KIND_RATIO[work.kind]
         extra = {"peak_sustained": round(ps, 2), "frac_sustained": round(ach / ps, 4)}
+    if work.bound == "tensor":
+        r = KIND_RATIO[work.kind]
+        den = {"datasheet": {"peak": DATASHEET_BF16_TFLOPS * r, "frac": round(ach / (DATASHEET_BF16_TFLOPS * r), 4)}}
+        mhz = (clocks or {}).get("sm_mhz")
+        if mhz:
+            cn = 148 * BF16_FMA_PER_CLK_SM * r * 2 * mhz * 1e6 / 1e12
+            den["clock_normalised"] = {"peak": round(cn, 1), "sm_mhz": mhz, "frac": round(ach / cn, 4)}
+        extra["denominators"] = den
     return {"bound": work.bound, "achieved": round(ach, 2), "peak": round(peak, 2), "unit": unit,
             "frac": round(ach / peak, 4), **extra, "traffic": traffic, "kernel": work.kernel,
             "peak_source": pk["source"] + (" x nominal %s/bf16 ratio %.1f" % (work.kind, KIND_RATIO[work.kind])

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/gputests.log 2>&1; echo tests=$?
