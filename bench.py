@@ -369,6 +369,30 @@ def time_e2e(work, steps, warmup):
     return e0.elapsed_time(e1) / steps
 
 
+def sustained(work, seconds, sampler, fn=None):
+    """SURVEY §8(d)'s sustained figure: back-to-back steps for `seconds` (the board settles at its
+    power cap), timed in chunks of CUDA events; returns the median chunk's metric value and the NVML
+    clock record of the run.  `fn` replaces work.step (the cuBLAS anchor)."""
+    step = fn or work.step
+    chunk = 50
+    vals = []
+    sampler.samples = []
+    sampler.start()
+    t0 = time.time()
+    while time.time() - t0 < seconds:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(chunk):
+            step()
+        e1.record()
+        e1.synchronize()
+        vals.append(work.metric_value(e0.elapsed_time(e1) / chunk * 1e-3))
+    t1 = time.time()
+    sampler.stop()
+    return {"value": round(float(np.median(vals)), 2), "seconds": round(t1 - t0, 2), "chunks": len(vals),
+            "steps_per_chunk": chunk, "clocks": sampler.summary(t0, t1)}
+
+
 def torch_matmul_anchor(work, steps):
     """same-run cuBLAS context for C3: torch.matmul on the bench's own bf16 A, B."""
     A, Bt = work.A, work.B.t()
@@ -556,6 +580,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="tcx", choices=["tcx", "reference"])
+    ap.add_argument("--sustained-s", type=float, default=4.0, help="seconds of the back-to-back sustained run (0 = skip)")
     ap.add_argument("--config", default="c3", choices=["c3", "c3tf32", "c4", "c5", "c1", "c4sp", "c3sptf32", "c3f16acc"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -643,6 +668,14 @@ def main():
         line["context"] = {"torch_matmul_bf16_tflops_same_run": torch_matmul_anchor(work, args.steps),
                            "note": "cuBLAS via torch.matmul(A, B^T) on the same bf16 A, B, bf16 output (no C): "
                                    "context only, not part of the step"}
+        if args.sustained_s > 0:
+            # 4 s back to back at the power cap, ours and the cuBLAS anchor, beside the burst value
+            Bt = work.B.t()
+            line["sustained"] = {"tcx": sustained(work, args.sustained_s, sampler),
+                                 "torch_matmul_bf16": sustained(work, args.sustained_s, sampler,
+                                                                fn=lambda: torch.matmul(work.A, Bt)),
+                                 "note": "median of 50-step chunks over the run; MEASURED_PEAKS bf16_tflops_sustained "
+                                         "is the same method on torch.matmul"}
         also = {}
         # lightest first: the launch-bound C1 is clock-sensitive and the power-capped 2:4 runs leave
         # the board hot (C1 measured after C5 ran at ~850 MHz)

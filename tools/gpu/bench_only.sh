@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > /dev/null
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$?
-timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref=$?
