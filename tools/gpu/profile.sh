@@ -2,7 +2,7 @@
 # usage: bash tools/gpu/profile.sh <tag>
 mkdir -p gpurun_out
 TAG=${1:-r01}
-BENCH="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
+BENCH="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --sustained-s 0"
 $BENCH > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm_|tiles|sp24|fill_c" --csv \
     --log-file gpurun_out/${TAG}_launches.csv $BENCH > gpurun_out/ncu_launch.log 2>&1
