@@ -177,3 +177,9 @@ def test_numeric_probe_report():
             t = fr["paper_tables"]
             assert t["PAPER3_init_low/mul"]["mean_abs_err_vs_exact"] == 0.0
             assert t["PAPER3_init_low/mul"]["mean_abs_err_vs_cpu_fp32"] == 0.0
+    # the classifier's result (DESIGN.md §7 finding 2): one model of the family reproduces every
+    # probed element, the same for mma.sync and tcgen05
+    for fmt in FMTS:
+        obs = {fam: fr["observed"] for fam, fr in rep[fmt]["families"].items()}
+        assert all(obs.values()), (fmt, obs)
+        assert len(set(obs.values())) == 1, (fmt, obs)
