@@ -571,9 +571,11 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
   if (a.max_ctas > 0 && a.max_ctas / CL < max_clusters) max_clusters = a.max_ctas / CL > 0 ? a.max_ctas / CL : 1;
   if (clusters > max_clusters) clusters = max_clusters;
   cfg.gridDim = dim3((unsigned)(clusters * CL));
-  if (getenv("TCX_DEBUG_LAUNCH"))
+#if TCX_WATCHDOG
+  if (getenv("TCX_DEBUG_LAUNCH"))   // debug library: print the launch shape
     fprintf(stderr, "tcx_gemm: grid %u CTAs, cluster %d (pairs %dx%d), %lld cluster tiles\n", cfg.gridDim.x, CL, PM, PN,
             (long long)(((m_tiles + PM - 1) / PM) * ((n_tiles + PN - 1) / PN)));
+#endif
   const uint32_t idesc = make_idesc(KIND, a_fmt, BM * CG, BN);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
                                   a.C ? 1 : 0, idesc, a.group_m != 0 ? a.group_m : GROUP_M, a.fault, a.trace,
