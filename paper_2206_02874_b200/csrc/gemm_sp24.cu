@@ -91,7 +91,10 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64
   const int64_t first = g * g_tiles;
   const int64_t gm = major - first < g_tiles ? major - first : g_tiles;
   const int64_t r = tile - g * per_group;
-  const int64_t a = first + r % gm, b = r / gm;
+  const int64_t a = first + r % gm;
+  // serpentine: odd groups sweep the minor dimension backwards, so a group starts on the operand
+  // tiles the previous group read last (still in L2)
+  const int64_t b = (g & 1) ? minor - 1 - r / gm : r / gm;
   mt = by_m ? a : b;
   nt = by_m ? b : a;
 }

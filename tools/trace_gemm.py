@@ -26,7 +26,8 @@ def tile_coords(t, m_tiles, n_tiles, g):
     first = grp * gt
     gm = np.minimum(major - first, gt)
     r = t - grp * per
-    a, b = first + r % gm, r // gm
+    a = first + r % gm
+    b = np.where(grp & 1, minor - 1 - r // gm, r // gm)          # serpentine (gemm_dense.cu)
     return (a, b) if by_m else (b, a)
 
 
