@@ -9,8 +9,9 @@ A step is one call of the hot path on its config's synthetic input, resident in 
   c5     2:4 sparse FP16 GEMM M=65536, N=K=16384, C FP32 zeros                        (configs[4])
   c1     4096 m16n8k16 FP16 tiles (HBM-bound; GB/s)                                   (configs[0])
 At N=1 the default run also measures c3tf32 / c4 / c5 / c1 on rank 0 ("also" key).
-Multi-GPU (torchrun): rows of A, C, D are sharded across ranks (strong scaling, total work
-fixed); B is replicated by one NCCL broadcast before timing; time = max over ranks.
+Multi-GPU (torchrun): rows of A, C, D are sharded across ranks — by default weak scaling (each
+rank one config-sized row block of an N-times taller problem, per-GPU work fixed); --scaling strong
+splits the config itself.  B is replicated by one NCCL broadcast before timing; time = max over ranks.
 
 --impl reference times the CPU oracle (oracle/, exact Kulisch accumulation) on a bounded sample
 of the same workload, on the host cores (rank 0 only).
@@ -124,11 +125,15 @@ class ClockSampler:
 class Work:
     """one config on this rank: inputs resident in HBM, step() launches the hot path once."""
 
-    def __init__(self, cfg, rank, world, dev, seed=0):
+    def __init__(self, cfg, rank, world, dev, seed=0, scaling="strong"):
         import tcxgen
         import paper_2206_02874_b200 as tcx
         self.tcx, self.cfg, self.dev = tcx, cfg, dev
         self.rank, self.world = rank, world
+        # weak scaling (N > 1): every rank owns a full config-sized row block of an N-times taller
+        # problem (its rows drawn with seed + 1000 * rank); strong: the config itself split by rows
+        self.weak = scaling == "weak" and world > 1
+        rs = seed + 1000 * rank if self.weak else seed
         g = tcxgen
         if cfg in ("c3", "c3tf32"):
             M = N = K = 8192
@@ -136,7 +141,7 @@ class Work:
             self.kind = fmt
             self.shape = (M, N, K)
             m0, m1 = self._rows(M)
-            self.A = g.normal_matrix((M, K), fmt, seed, g.STREAM_A, dev)[m0:m1].contiguous()
+            self.A = g.normal_matrix((M, K), fmt, rs, g.STREAM_A, dev)[m0:m1].contiguous()
             self.B = self._bcast(lambda: g.normal_matrix((N, K), fmt, seed, g.STREAM_B, dev))
             self.C = torch.zeros(m1 - m0, N, dtype=torch.float32, device=dev)
             self.D = torch.empty(m1 - m0, N, dtype=torch.float32, device=dev)
@@ -151,7 +156,7 @@ class Work:
             self.kind = "f16acc"
             self.shape = (M, N, K)
             m0, m1 = self._rows(M)
-            self.A = g.normal_matrix((M, K), "f16", seed, g.STREAM_A, dev)[m0:m1].contiguous()
+            self.A = g.normal_matrix((M, K), "f16", rs, g.STREAM_A, dev)[m0:m1].contiguous()
             self.B = self._bcast(lambda: g.normal_matrix((N, K), "f16", seed, g.STREAM_B, dev))
             self.C = torch.zeros(m1 - m0, N, dtype=torch.float16, device=dev)
             self.D = torch.empty(m1 - m0, N, dtype=torch.float16, device=dev)
@@ -165,9 +170,9 @@ class Work:
             self.kind = "s8"
             self.shape = (M, N, K)
             m0, m1 = self._rows(M)
-            self.A = g.int8_matrix((M, K), seed, g.STREAM_A, dev)[m0:m1].contiguous()
+            self.A = g.int8_matrix((M, K), rs, g.STREAM_A, dev)[m0:m1].contiguous()
             self.B = self._bcast(lambda: g.int8_matrix((N, K), seed, g.STREAM_B, dev))
-            self.C = g.int32_matrix((M, N), seed, g.STREAM_C, device=dev)[m0:m1].contiguous()
+            self.C = g.int32_matrix((M, N), rs, g.STREAM_C, device=dev)[m0:m1].contiguous()
             self.D = torch.empty(m1 - m0, N, dtype=torch.int32, device=dev)
             self.flops = 2.0 * (m1 - m0) * N * K
             self.alg_bytes = self.A.numel() + self.B.numel() + 8 * (m1 - m0) * N
@@ -179,7 +184,7 @@ class Work:
             self.kind = "sp16"
             self.shape = (M, N, K)
             m0, m1 = self._rows(M)
-            vals, meta = g.sp24_problem(M, K, seed, "f16", dev)
+            vals, meta = g.sp24_problem(M, K, rs, "f16", dev)
             self.vals = vals[m0:m1].contiguous()
             meta = meta[m0:m1].contiguous()
             del vals
@@ -201,13 +206,13 @@ class Work:
             self.shape = (M, N, K)
             m0, m1 = self._rows(M)
             if cfg == "c4sp":
-                vals, meta = g.sp24_problem_i8(M, K, seed, dev)
+                vals, meta = g.sp24_problem_i8(M, K, rs, dev)
                 self.B = self._bcast(lambda: g.int8_matrix((N, K), seed, g.STREAM_B, dev))
-                self.C = g.int32_matrix((M, N), seed, g.STREAM_C, device=dev)[m0:m1].contiguous()
+                self.C = g.int32_matrix((M, N), rs, g.STREAM_C, device=dev)[m0:m1].contiguous()
                 self.D = torch.empty(m1 - m0, N, dtype=torch.int32, device=dev)
                 ab, esize = tcx.S8, 1
             else:
-                vals, meta = g.sp12_problem_tf32(M, K, seed, dev)
+                vals, meta = g.sp12_problem_tf32(M, K, rs, dev)
                 self.B = self._bcast(lambda: g.normal_matrix((N, K), "tf32", seed, g.STREAM_B, dev))
                 self.C = torch.zeros(m1 - m0, N, dtype=torch.float32, device=dev)
                 self.D = torch.empty(m1 - m0, N, dtype=torch.float32, device=dev)
@@ -255,6 +260,8 @@ class Work:
             raise ValueError(cfg)
 
     def _rows(self, M):
+        if self.weak:
+            return 0, M
         from paper_2206_02874_b200.dist import row_shard
         return row_shard(M, self.world, self.rank)
 
@@ -580,6 +587,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="tcx", choices=["tcx", "reference"])
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N > 1: weak = every rank a full config-sized row block (default); strong = the config split by rows")
     ap.add_argument("--sustained-s", type=float, default=4.0, help="seconds of the back-to-back sustained run (0 = skip)")
     ap.add_argument("--config", default="c3", choices=["c3", "c3tf32", "c4", "c5", "c1", "c4sp", "c3sptf32", "c3f16acc"])
     ap.add_argument("--no-extras", action="store_true")
@@ -607,7 +616,7 @@ def main():
         cb = oracle_sample(args.config, seconds=10.0)
         line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": cb["unit"], "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": {"c4": "s8", "c3tf32": "tf32", "c5": "f16"}.get(args.config, "bf16"),
+                "scaling": "weak", "vs_baseline": None, "dtype": {"c4": "s8", "c3tf32": "tf32", "c5": "f16"}.get(args.config, "bf16"),
                 "data": "synthetic (seeded SplitMix64 / Box-Muller, tcxgen)",
                 "config": {"workload": cfg_names[args.config]},
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -625,7 +634,7 @@ def main():
     tcx.lib()
     pk = peaks()
 
-    work = Work(args.config, rank, world, dev)
+    work = Work(args.config, rank, world, dev, scaling=args.scaling)
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
@@ -653,13 +662,14 @@ def main():
 
     line = {"metric": metric, "value": round(value, 3), "unit": work.unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak",
+            "scaling": "weak" if (world == 1 or work.weak) else "strong",
             "vs_baseline": None,
             "dtype": {"c3": "bf16", "c3tf32": "tf32", "c4": "s8", "c5": "f16", "c1": "f16", "c4sp": "s8",
                       "c3sptf32": "tf32", "c3f16acc": "f16"}[args.config],
             "data": "synthetic (seeded SplitMix64 / Box-Muller, tcxgen; generated on device)",
             "config": {"workload": cfg_names[args.config], "shape": list(work.shape),
-                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"row-shard x{world} ({'weak: each rank one config-sized row block, rows seeded per rank' if work.weak else 'strong: the config split by rows'})"
+                                       if world > 1 else "single GPU"),
                        "l2": "inputs+outputs per step > 126 MiB L2 (no reuse across steps)" if args.config != "c1"
                        else "64 rotating batch copies (470 MB) > L2"},
             "roofline": roofline(work, ms, pk, clocks), "clocks": clocks, "gpu_launches": launches,
