@@ -216,13 +216,11 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
   if (!ok) return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm: (ab=%d, cd=%d) not supported", ab, cd);
   tcx_status st = check_gemm_common("tcx_gemm", ab, cd, M, N, K, A, lda, B, ldb, C, ldc, D, ldd, K);
   if (st != TCX_OK || M == 0 || N == 0) return st;
-  if (opts && opts->cta_group != 0 && opts->cta_group != 1 && opts->cta_group != 2)
-    return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: cta_group must be 0, 1 or 2");
-  DevInfo dev;
-  st = current_device(&dev);
-  if (st != TCX_OK) return st;
+  // every argument check precedes the device query (host-testable without a GPU)
   GemmArgs g{ab, cd, M, N, K, A, lda, B, ldb, C, ldc, D, ldd, nullptr, 2, 0, 0, 0};
   if (opts) {
+    if (opts->cta_group != 0 && opts->cta_group != 1 && opts->cta_group != 2)
+      return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: cta_group must be 0, 1 or 2");
     if (opts->cta_group) g.cta_group = opts->cta_group;
     g.max_ctas = opts->max_ctas;
     g.group_m = opts->group_m;
@@ -240,6 +238,9 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
     g.fault = opts->reserved[0];   // fault injection exists only in the debug library
 #endif
   }
+  DevInfo dev;
+  st = current_device(&dev);
+  if (st != TCX_OK) return st;
 #if TCX_WATCHDOG
   g.trace = g_trace;
   g.trace_cap = g_trace_cap;
@@ -310,9 +311,6 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
   tcx_status st = check_gemm_common("tcx_gemm_sp24", ab, cd, M, N, K, A_vals, lda_vals, B, ldb, C, ldc, D, ldd, K / 2);
   if (st != TCX_OK) return st;
   if (!meta_hw || !aligned16(meta_hw)) return set_error(TCX_ERR_MISALIGNED, "tcx_gemm_sp24: meta_hw NULL or misaligned");
-  DevInfo dev;
-  st = current_device(&dev);
-  if (st != TCX_OK) return st;
   GemmArgs g{ab, cd, M, N, K, A_vals, lda_vals, B, ldb, C, ldc, D, ldd, meta_hw, 2, 0, 0, 0};
   if (opts) {
     if (opts->cta_group == 1 || opts->cta_group == 2) g.cta_group = opts->cta_group;
@@ -329,6 +327,9 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
   }
   if (g.cta_group == 2 && M % 256)
     return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: the CTA-pair kernel needs M %% 256 == 0 (use cta_group=1)");
+  DevInfo dev;
+  st = current_device(&dev);
+  if (st != TCX_OK) return st;
   return launch_gemm_sp24(g, dev, (cudaStream_t)stream);
 }
 
