@@ -678,14 +678,6 @@ def main():
         line["context"] = {"torch_matmul_bf16_tflops_same_run": torch_matmul_anchor(work, args.steps),
                            "note": "cuBLAS via torch.matmul(A, B^T) on the same bf16 A, B, bf16 output (no C): "
                                    "context only, not part of the step"}
-        if args.sustained_s > 0:
-            # 4 s back to back at the power cap, ours and the cuBLAS anchor, beside the burst value
-            Bt = work.B.t()
-            line["sustained"] = {"tcx": sustained(work, args.sustained_s, sampler),
-                                 "torch_matmul_bf16": sustained(work, args.sustained_s, sampler,
-                                                                fn=lambda: torch.matmul(work.A, Bt)),
-                                 "note": "median of 50-step chunks over the run; MEASURED_PEAKS bf16_tflops_sustained "
-                                         "is the same method on torch.matmul"}
         also = {}
         # lightest first: the launch-bound C1 is clock-sensitive and the power-capped 2:4 runs leave
         # the board hot (C1 measured after C5 ran at ~850 MHz)
@@ -708,6 +700,15 @@ def main():
             except Exception as e:  # report, never hide
                 also[extra] = {"error": f"{type(e).__name__}: {e}"}
         line["also"] = also
+        if args.sustained_s > 0:
+            # 4 s back to back at the power cap, ours and the cuBLAS anchor, beside the burst value
+            # (after the extras: it leaves the board hot, and the launch-bound C1 is clock-sensitive)
+            Bt = work.B.t()
+            line["sustained"] = {"tcx": sustained(work, args.sustained_s, sampler),
+                                 "torch_matmul_bf16": sustained(work, args.sustained_s, sampler,
+                                                                fn=lambda: torch.matmul(work.A, Bt)),
+                                 "note": "median of 50-step chunks over the run; MEASURED_PEAKS bf16_tflops_sustained "
+                                         "is the same method on torch.matmul"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = oracle_sample(args.config, seconds=10.0)
         line["cpu_baseline"] = {k: (round(cb[k], 6) if isinstance(cb[k], float) else cb[k])
