@@ -84,8 +84,10 @@ tcx_status tcx_mma_tiles(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, int64_
  * are FP16, ldc*2 / ldd*2 multiples of 16 bytes, and C is the MMA's own C operand — loaded into
  * the tensor-memory accumulator before the first MMA — not an epilogue add).
  * Any M, N >= 1 and K >= 1 subject to the alignment rules (ragged tiles are handled by
- * TMA out-of-bounds zero fill and predicated stores).  M == 0 or N == 0 is a no-op;
- * K == 0 gives D = C.
+ * TMA out-of-bounds zero fill and TMA-store clipping).  M == 0 or N == 0 is a no-op;
+ * K == 0 gives D = C.  D may alias C (in place).  Launched with programmatic dependent launch:
+ * the kernel's setup overlaps the previous kernel in the stream, its first global access waits
+ * for that kernel's completion, so stream order is unchanged.
  * ------------------------------------------------------------------------------------- */
 tcx_status tcx_gemm(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
                     const void* A, int64_t lda, const void* B, int64_t ldb,
@@ -106,8 +108,18 @@ typedef struct {
                    /* of a row and B across the pairs_m pairs of a column; elsewhere the pairs load */
                    /* their own operands.  1 or 2 each; 0 = default 1.  Results are bit-identical  */
                    /* to the default.                                                               */
-  int reserved[2];
+  int reserved[2]; /* 0.  reserved[0] = 1 in the debug library (libtcx_debug.so) only: the dense
+                      producer drops one TMA load (fault injection for the watchdog tests);
+                      the product library ignores it */
 } tcx_gemm_opts;
+/* opts == NULL -> all defaults.  Option errors (cta_group not 0/1/2, tile_n not 0/256/512,
+ * pairs outside 1..2 or combined with cta_group 1 / tile_n 512) -> TCX_ERR_INVALID_VALUE, checked
+ * with every other argument before any device query. */
+tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
+                       const void* A, int64_t lda, const void* B, int64_t ldb,
+                       const void* C, int64_t ldc, void* D, int64_t ldd,
+                       const tcx_gemm_opts* opts, void* stream);
+
 /* Debug library only (libtcx_debug.so; the product returns TCX_ERR_UNSUPPORTED): per-tile timeline
  * of later tcx_gemm / tcx_gemm_ex launches (CTA-pair kernel).  d_buf: device buffer of
  * 4 * capacity uint64 (caller-owned, NULL = off); tile record i (cluster tile i of the launch's raster):
@@ -115,11 +127,6 @@ typedef struct {
  *   [2] = when its last MMA was committed, [3] = when the epilogue issued its last store.
  * Records past `capacity` are dropped.  Used to study L2 reuse across concurrent tiles. */
 tcx_status tcx_debug_trace(void* d_buf, int64_t capacity);
-
-tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
-                       const void* A, int64_t lda, const void* B, int64_t ldb,
-                       const void* C, int64_t ldc, void* D, int64_t ldd,
-                       const tcx_gemm_opts* opts, void* stream);
 
 /* ---------------------------------------------------------------------------------------
  * 2:4 structured sparsity: "for every four consecutive elements along
