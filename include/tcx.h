@@ -199,12 +199,18 @@ tcx_status tcx_round_tf32(const float* in, float* out, int64_t n, void* stream);
  *   TCX_PROBE_TMA_LOAD     ilp cp.async.bulk.tensor.2d loads of an m-row x n-byte box (L2-resident
  *                          16 MiB source) per mbarrier wait, one thread per CTA: operand staging
  *   TCX_PROBE_TC05_CP      ilp tcgen05.cp.cta_group::1.128x128b (2 KiB smem -> TMEM) per commit
+ *   TCX_PROBE_TMA_MULTICAST  clusters of cta_group (1..8) CTAs that all need the same ilp boxes
+ *                          (m rows x n bytes) per wait: k = 1 -> box j is loaded once, by CTA
+ *                          j % cta_group, with .multicast::cluster to every CTA of the cluster;
+ *                          k = 0 -> every CTA loads every box itself (unicast).  Throughput =
+ *                          bytes delivered per clk per SM (the dense/sparse multicast groups).
  * Synchronous; allocates and frees its own scratch.  Shapes not implemented ->
  * TCX_ERR_UNSUPPORTED.
  * ------------------------------------------------------------------------------------- */
 typedef enum { TCX_PROBE_MMA_SYNC = 0, TCX_PROBE_MMA_SP_SYNC = 1, TCX_PROBE_TC05 = 2,
                TCX_PROBE_TC05_SP = 3, TCX_PROBE_LDMATRIX = 4, TCX_PROBE_LDSHARED = 5,
-               TCX_PROBE_TMEM_LD = 6, TCX_PROBE_TMA_LOAD = 7, TCX_PROBE_TC05_CP = 8 } tcx_probe_kind;
+               TCX_PROBE_TMEM_LD = 6, TCX_PROBE_TMA_LOAD = 7, TCX_PROBE_TC05_CP = 8,
+               TCX_PROBE_TMA_MULTICAST = 9 } tcx_probe_kind;
 typedef struct {
   int kind;          /* tcx_probe_kind */
   int ab, cd;        /* tcx_dtype */

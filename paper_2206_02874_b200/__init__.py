@@ -267,7 +267,7 @@ def round_tf32(x, out=None):
 
 # ---------------------------------------------------------------------------------------- probe
 PROBE_KINDS = {"mma_sync": 0, "mma_sp_sync": 1, "tc05": 2, "tc05_sp": 3, "ldmatrix": 4, "ld_shared": 5,
-               "tmem_ld": 6, "tma_load": 7, "tc05_cp": 8}
+               "tmem_ld": 6, "tma_load": 7, "tc05_cp": 8, "tma_multicast": 9}
 
 
 def probe(kind="mma_sync", ab=F16, cd=F32, m=16, n=8, k=16, cta_group=1, warps=1, ilp=1, iters=1024,

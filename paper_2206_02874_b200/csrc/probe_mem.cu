@@ -213,6 +213,44 @@ __global__ void __launch_bounds__(32, 1) probe_tma_kernel(const __grid_constant_
   ns[blockIdx.x * 32] = (long long)(g1 - g0);
 }
 
+// ---------------------------------------------------------------- TMA multicast (clusters)
+// every CTA of a cluster needs the same ilp boxes per iteration.  mc: box s is issued once, by the
+// CTA of cluster rank s % cs, multicast to all cs CTAs; else every CTA loads every box itself.
+// Each CTA's barrier expects ilp boxes either way (delivered bytes per CTA are equal).
+__global__ void __launch_bounds__(32, 1) probe_tma_mc_kernel(const __grid_constant__ CUtensorMap tm, int iters, int ilp,
+                                                             int box_rows, uint32_t box_bytes, int rows_total, int mc,
+                                                             long long* cycles, long long* ns) {
+  extern __shared__ uint8_t dyn[];
+  uint8_t* buf = (uint8_t*)(((uintptr_t)dyn + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  const uint32_t cs = cluster_nctarank(), r = cluster_ctarank();
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  cluster_sync();                                   // every barrier armed before any multicast lands
+  if (threadIdx.x == 0) {
+    const uint16_t mask = (uint16_t)((1u << cs) - 1);
+    uint32_t phase = 0;
+    long long t0 = 0; uint64_t g0 = 0;
+    int y = (int)((blockIdx.x / cs) * 97) % (rows_total - box_rows);   // the same boxes per cluster
+    for (int it = -4; it < iters; ++it) {
+      if (it == 0) { t0 = clock64(); g0 = gtimer(); }
+      mbar_arrive_expect_tx(&bar, (uint32_t)ilp * box_bytes);
+      for (int s = 0; s < ilp; ++s) {
+        if (!mc) tma_load_2d(buf + s * box_bytes, &tm, &bar, 0, y);
+        else if ((uint32_t)s % cs == r) tma_load_2d_mc(buf + s * box_bytes, &tm, &bar, 0, y, mask);
+        y += box_rows;
+        if (y + box_rows > rows_total) y = 0;
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+    }
+    const long long t1 = clock64();
+    const uint64_t g1 = gtimer();
+    cycles[blockIdx.x * 32] = t1 - t0;
+    ns[blockIdx.x * 32] = (long long)(g1 - g0);
+  }
+  cluster_sync();                                   // no CTA leaves while peers still write into it
+}
+
 // ---------------------------------------------------------------- tcgen05.cp (smem -> TMEM)
 // the sparse path's metadata staging: ILP tcgen05.cp.cta_group::1.128x128b (2 KiB each) into
 // distinct TMEM columns, then tcgen05.commit -> mbarrier wait.
@@ -300,6 +338,7 @@ tcx_status run_probe_mem(const DevInfo& dev, const tcx_probe_config* cfg, tcx_pr
   tcx_status st = TCX_OK;
   double bytes_per_warp_iter = 0;
   int warps_eff = warps;              // timing slots per CTA (1 for the single-thread TMA / cp probes)
+  int launched = nsm;                 // CTAs actually timed (the multicast probe rounds to clusters)
   void* tma_src = nullptr;
   std::vector<double> per_iter, per_ns;
   for (int rep = 0; rep < reps && st == TCX_OK; ++rep) {
@@ -359,6 +398,44 @@ tcx_status run_probe_mem(const DevInfo& dev, const tcx_probe_config* cfg, tcx_pr
       bytes_per_warp_iter = (double)rows * inner * ilp;
       probe_tma_kernel<<<nsm, 32, smem>>>(tm, iters, ilp, rows, (uint32_t)(rows * inner), 4096, d_cyc, d_ns);
       warps_eff = 1;
+    } else if (cfg->kind == TCX_PROBE_TMA_MULTICAST) {
+      const int rows = cfg->m > 0 ? cfg->m : 128, inner = cfg->n > 0 ? cfg->n : 128;
+      const int cs = cfg->cta_group > 0 ? cfg->cta_group : 1;
+      if (rows > 256 || inner > 256 || inner % 16 || rows * inner * ilp > 200 * 1024 || cs > 8 || (cs & (cs - 1)) ||
+          (cfg->k && ilp % cs)) {
+        st = set_error(TCX_ERR_UNSUPPORTED, "tcx_probe: TMA multicast box m <= 256, n <= 256 (x16), "
+                                            "ilp*box <= 200 KiB, cluster 1/2/4/8, ilp %% cluster == 0");
+        break;
+      }
+      if (!tma_src) {
+        if (cudaMalloc(&tma_src, 4096u * 4096u) != cudaSuccess) { st = set_error(TCX_ERR_CUDA, "probe: cudaMalloc"); break; }
+        cudaMemset(tma_src, 1, 4096u * 4096u);
+      }
+      CUtensorMap tm;
+      st = make_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, tma_src, 4096, 4096, 4096, (uint32_t)inner, (uint32_t)rows,
+                        CU_TENSOR_MAP_SWIZZLE_NONE);
+      if (st != TCX_OK) break;
+      const int smem = rows * inner * ilp + 1024;
+      cudaFuncSetAttribute(probe_tma_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaLaunchConfig_t lc = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      lc.blockDim = dim3(32);
+      lc.dynamicSmemBytes = smem;
+      lc.attrs = at; lc.numAttrs = 1;
+      // co-resident clusters only, so every measured CTA loads while all others do
+      int ncl = nsm / cs > 0 ? nsm / cs : 1;
+      lc.gridDim = dim3((unsigned)(ncl * cs));
+      int fit = 0;
+      if (cudaOccupancyMaxActiveClusters(&fit, probe_tma_mc_kernel, &lc) == cudaSuccess && fit > 0 && fit < ncl) ncl = fit;
+      lc.gridDim = dim3((unsigned)(ncl * cs));
+      launched = ncl * cs;
+      bytes_per_warp_iter = (double)rows * inner * ilp;
+      le = cudaLaunchKernelEx(&lc, probe_tma_mc_kernel, tm, iters, ilp, rows, (uint32_t)(rows * inner), 4096,
+                              cfg->k ? 1 : 0, d_cyc, d_ns);
+      if (le != cudaSuccess) { st = set_error(TCX_ERR_CUDA, "probe multicast launch: %s", cudaGetErrorString(le)); break; }
+      warps_eff = 1;
     } else if (cfg->kind == TCX_PROBE_TC05_CP) {
       bytes_per_warp_iter = 2048.0 * ilp;
       probe_tc05_cp_kernel<<<nsm, 128>>>(iters, ilp, d_cyc, d_ns);
@@ -375,7 +452,7 @@ tcx_status run_probe_mem(const DevInfo& dev, const tcx_probe_config* cfg, tcx_pr
     cudaMemcpy(cyc.data(), d_cyc, cyc.size() * sizeof(long long), cudaMemcpyDeviceToHost);
     cudaMemcpy(nsv.data(), d_ns, nsv.size() * sizeof(long long), cudaMemcpyDeviceToHost);
     std::vector<double> c2, n2;
-    for (int b = 0; b < nsm; ++b)
+    for (int b = 0; b < launched; ++b)
       for (int w = 0; w < warps_eff; ++w) { c2.push_back((double)cyc[b * 32 + w]); n2.push_back((double)nsv[b * 32 + w]); }
     per_iter.push_back(*std::max_element(c2.begin(), c2.end()) / iters);   // the slowest warp bounds the SM
     per_ns.push_back(*std::max_element(n2.begin(), n2.end()) / iters);

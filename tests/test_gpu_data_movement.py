@@ -72,6 +72,20 @@ def test_tma_and_tc05_cp_probes():
     assert c1["latency_cycles"] > 0 and c8["fma_per_clk_per_sm"] > c1["fma_per_clk_per_sm"]
 
 
+def test_tma_multicast_probe():
+    """clusters whose CTAs all need the same boxes: multicast (each box fetched once, delivered to
+    every CTA) and unicast (every CTA fetches every box) deliver the same bytes per CTA.  Both must
+    complete every wait (a lost multicast signal would hang) and deliver at a sane rate; which one
+    is faster is a measurement (DESIGN.md §7 data movement), not asserted."""
+    for cs in (2, 4, 8):
+        uc = _p("tma_multicast", m=128, n=128, ilp=8, cta_group=cs, k=0, num_sms=148)
+        mc = _p("tma_multicast", m=128, n=128, ilp=8, cta_group=cs, k=1, num_sms=148)
+        assert uc["latency_cycles"] > 0 and mc["latency_cycles"] > 0
+        assert uc["fma_per_clk_per_sm"] > 10 and mc["fma_per_clk_per_sm"] > 10, (cs, uc, mc)
+    with pytest.raises(tcx.TcxError):
+        _p("tma_multicast", m=128, n=128, ilp=6, cta_group=4, k=1)      # ilp must split over the cluster
+
+
 def test_data_movement_sweep_report():
     rep = {"units": {"latency": "cycles per iteration (clock64)", "throughput": "bytes/clk/SM"},
            "paper_A100_context": {
@@ -112,6 +126,13 @@ def test_data_movement_sweep_report():
         rep["tma_load"][f"box{rows}x{inner}B"] = row
     rep["tc05_cp_128x128b"] = {f"ilp{ilp}": [round(r["latency_cycles"], 1), round(r["fma_per_clk_per_sm"], 2)]
                                 for ilp in (1, 2, 4, 8) for r in [_p("tc05_cp", ilp=ilp, repeats=2)]}
+    rep["tma_multicast"] = {}
+    for cs in (1, 2, 4, 8):
+        for mcast in ((0, 1) if cs > 1 else (0,)):
+            for nsm in (cs, 148):
+                r = _p("tma_multicast", m=128, n=128, ilp=8, cta_group=cs, k=mcast, num_sms=nsm, repeats=2)
+                rep["tma_multicast"][f"cluster{cs}_{'mc' if mcast else 'uc'}_sms{nsm}"] = [
+                    round(r["latency_cycles"], 1), round(r["fma_per_clk_per_sm"], 2)]
     out = os.environ.get("TCX_REPORT_DIR", "gpurun_out")
     os.makedirs(out, exist_ok=True)
     with open(os.path.join(out, "data_movement_report.json"), "w") as f:
