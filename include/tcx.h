@@ -121,7 +121,8 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
                        const tcx_gemm_opts* opts, void* stream);
 
 /* Debug library only (libtcx_debug.so; the product returns TCX_ERR_UNSUPPORTED): per-tile timeline
- * of later tcx_gemm / tcx_gemm_ex launches (CTA-pair kernel).  d_buf: device buffer of
+ * of later tcx_gemm / tcx_gemm_ex / tcx_gemm_sp24(_ex) launches (CTA-pair kernels; for the sparse
+ * M-wide tile [1] is the first half-0 MMA).  d_buf: device buffer of
  * 4 * capacity uint64 (caller-owned, NULL = off); tile record i (cluster tile i of the launch's raster):
  *   [0] = pair id << 32 | tile index, [1] = %globaltimer ns when the tile's first MMA issued,
  *   [2] = when its last MMA was committed, [3] = when the epilogue issued its last store.

@@ -327,6 +327,10 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
   }
   if (g.cta_group == 2 && M % 256)
     return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: the CTA-pair kernel needs M %% 256 == 0 (use cta_group=1)");
+#if TCX_WATCHDOG
+  g.trace = g_trace;
+  g.trace_cap = g_trace_cap;
+#endif
   DevInfo dev;
   st = current_device(&dev);
   if (st != TCX_OK) return st;

@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmC,
                  const __grid_constant__ CUtensorMap tmD, int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc,
-                 int group_m) {
+                 int group_m, uint64_t* trace, int64_t trace_cap) {
   using C_ = SpCfg<CG, KIND, MW>;
   constexpr int KL = C_::KL;
   constexpr int MH = C_::MH;
@@ -255,6 +255,13 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           for (int64_t kb = 0; kb < L; ++kb) {
             mbar_wait(&sm->full[stage], phase);
             tc05_fence_after();
+#if TCX_WATCHDOG
+            if (kb == 0 && trace && tile < trace_cap && elect_one()) {   // debug tile timeline
+              trace[4 * tile] = ((uint64_t)cluster_id << 32) | (uint64_t)tile;
+              trace[4 * tile + 1] = globaltimer_ns();
+            }
+            __syncwarp();
+#endif
             if (elect_one()) issue(stage, 0, kb, tmem_base);
             __syncwarp();
             if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
@@ -282,6 +289,17 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             for (int h = 0; h < MH; ++h) issue(stage, h, kb, MW ? tmem_base + h * BN : tmem_d);
             commit_slot(&sm->empty[stage]);
             if (kb == k_blocks - 1) commit_acc(&sm->tmem_full[acc]);
+#if TCX_WATCHDOG
+            if (trace && tile < trace_cap) {                      // debug tile timeline
+              if (!MW && kb == 0) {
+                trace[4 * tile] = ((uint64_t)cluster_id << 32) | (uint64_t)tile;
+                trace[4 * tile + 1] = globaltimer_ns();
+              }
+              if (kb == k_blocks - 1) trace[4 * tile + 2] = globaltimer_ns();
+            }
+#else
+            (void)trace; (void)trace_cap;
+#endif
           }
           __syncwarp();
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
@@ -387,6 +405,12 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
         load_c(q + 2);
       }
+#if TCX_WATCHDOG
+      if (trace && e == 0 && lane == 0 && rank == 0) {
+        const int64_t tile = cluster_id + it * num_clusters;
+        if (tile < trace_cap) trace[4 * tile + 3] = globaltimer_ns();
+      }
+#endif
       if (MW) { acc_phase ^= 1; }
       else if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -456,7 +480,7 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   const uint32_t idesc = (1u << 2) | (cfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
                          ((uint32_t)((BM * CG) >> 4) << 24);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tE, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
-                                  a.C ? 1 : 0, idesc, a.group_m != 0 ? a.group_m : GROUP_M));
+                                  a.C ? 1 : 0, idesc, a.group_m != 0 ? a.group_m : GROUP_M, a.trace, a.trace_cap));
   count_launch();
   return TCX_OK;
 }

@@ -34,14 +34,19 @@ def tile_coords(t, m_tiles, n_tiles, g):
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
     g = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+    wide = len(sys.argv) > 3 and sys.argv[3] == "wide"      # c5: the 512 x 240 M-wide tile
     torch.cuda.set_device(0)
     w = bench.Work(cfg, 0, 1, torch.device("cuda", 0))
     tcx = w.tcx
     M, N, K = w.shape
-    m_tiles, n_tiles = (M + 255) // 256, (N + 255) // 256
+    if cfg.startswith("c5"):
+        m_tiles, n_tiles = M // (512 if wide else 256), (N + 239) // 240
+        step = lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, group_m=g, tile_m=512 if wide else 0)
+    else:
+        m_tiles, n_tiles = (M + 255) // 256, (N + 255) // 256
+        step = lambda: tcx.gemm(w.A, w.B, w.C, w.D, tf32=getattr(w, "tf32", False), group_m=g)
     T = m_tiles * n_tiles
     buf = torch.zeros(4 * T, dtype=torch.int64, device="cuda")
-    step = lambda: tcx.gemm(w.A, w.B, w.C, w.D, tf32=getattr(w, "tf32", False), group_m=g)
     for _ in range(3):
         step()
     tcx.debug_trace(buf)
@@ -77,8 +82,18 @@ def main():
            "A_sharers_start_spread_us": {"median": float(np.median(sa)), "p90": float(np.percentile(sa, 90)),
                                          "max": float(sa.max())} if len(sa) else None,
            "last_tile_end_spread_us": float(np.ptp([eend[pair == p].max() for p in np.unique(pair)]))}
+    # MMA idle between a pair's consecutive tiles (next first MMA - this tile's last commit)
+    gaps = []
+    for p in np.unique(pair):
+        idx = np.where(pair == p)[0]
+        idx = idx[np.argsort(start[idx])]
+        gaps += list(start[idx[1:]] - mend[idx[:-1]])
+    gaps = np.array(gaps)
+    rep["inter_tile_mma_gap_us"] = {"median": float(np.median(gaps)), "p90": float(np.percentile(gaps, 90))} if gaps.size else None
+    rep["mma_busy_fraction"] = float(dur.sum() / (dur.sum() + gaps.sum())) if gaps.size else None
+    rep["wide"] = wide
     print(json.dumps(rep))
-    np.save(os.path.join(os.environ.get("TCX_REPORT_DIR", "gpurun_out"), f"trace_{cfg}_g{g}.npy"), r)
+    np.save(os.path.join(os.environ.get("TCX_REPORT_DIR", "gpurun_out"), f"trace_{cfg}_g{g}{'_wide' if wide else ''}.npy"), r)
 
 
 if __name__ == "__main__":
