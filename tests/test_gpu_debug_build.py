@@ -132,3 +132,34 @@ print("OK")
         assert np.all(np.diff(s) > 0)                             # a pair's tiles run in order
     with pytest.raises(tcx.TcxError):
         tcx.debug_trace(torch.zeros(8, dtype=torch.int64, device="cuda"))
+
+
+def test_sparse_tile_trace(tmp_path):
+    """tcx_debug_trace on the 2:4 kernel (narrow and M-wide tiles): every tile recorded, in order."""
+    code = """
+import numpy as np, torch
+import tcxgen, paper_2206_02874_b200 as tcx
+dev = "cuda"
+M, N, K = 1024, 960, 512
+vals, meta = tcxgen.sp24_problem(M, K, 4, "f16", dev)
+B = tcxgen.normal_matrix((N, K), "f16", 4, tcxgen.STREAM_B, dev)
+hw = tcx.sp24_pack_meta(meta, M, K)
+out = {}
+for tm in (0, 512):
+    T = (M // (512 if tm else 256)) * (N // 240)
+    buf = torch.zeros(4 * T, dtype=torch.int64, device=dev)
+    tcx.debug_trace(buf)
+    tcx.gemm_sp24(vals, hw, B, None, tile_m=tm, max_ctas=4)
+    torch.cuda.synchronize()
+    tcx.debug_trace(None)
+    out[str(tm)] = buf.view(T, 4).cpu().numpy()
+np.savez("tr.npz", **out)
+print("OK")
+"""
+    r = _run(code, tmp_path)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-2000:]
+    z = np.load(tmp_path / "tr.npz")
+    for k in z.files:
+        t = z[k].astype(np.int64)
+        assert np.array_equal(t[:, 0] & 0xFFFFFFFF, np.arange(len(t))), k
+        assert np.all(t[:, 1] > 0) and np.all(t[:, 1] <= t[:, 2]) and np.all(t[:, 2] <= t[:, 3]), k
