@@ -82,7 +82,11 @@ class ClockSampler:
             try:
                 mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
                 rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.samples.append((time.time(), mhz, rs))
+                try:
+                    pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                except Exception:
+                    pw = None
+                self.samples.append((time.time(), mhz, rs, pw))
             except Exception:
                 pass
             time.sleep(0.005)
@@ -112,13 +116,15 @@ class ClockSampler:
                  getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 64): "hw_thermal_slowdown",
                  getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 128): "hw_power_brake_slowdown"}
         rs = set()
-        for _, _, r in inside:
+        for _, _, r, _ in inside:
             for bit, nm in names.items():
                 if r & bit:
                     rs.add(nm)
         mhz = [s[1] for s in inside]
+        pw = [s[3] for s in inside if s[3] is not None]
         return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(rs), "samples": len(inside)}
+                "reasons": sorted(rs), "samples": len(inside),
+                "power_w_median": round(statistics.median(pw), 1) if pw else None}
 
 
 # ----------------------------------------------------------------------------------- workloads
