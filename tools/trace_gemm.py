@@ -43,8 +43,9 @@ def main():
         m_tiles, n_tiles = M // (512 if wide else 256), (N + 239) // 240
         step = lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, group_m=g, tile_m=512 if wide else 0)
     else:
-        m_tiles, n_tiles = (M + 255) // 256, (N + 255) // 256
-        step = lambda: tcx.gemm(w.A, w.B, w.C, w.D, tf32=getattr(w, "tf32", False), group_m=g)
+        tn = 512 if wide else 256                            # dense: the 256 x 512 pair tile
+        m_tiles, n_tiles = (M + 255) // 256, (N + tn - 1) // tn
+        step = lambda: tcx.gemm(w.A, w.B, w.C, w.D, tf32=getattr(w, "tf32", False), group_m=g, tile_n=tn)
     T = m_tiles * n_tiles
     buf = torch.zeros(4 * T, dtype=torch.int64, device="cuda")
     for _ in range(3):
