@@ -139,7 +139,9 @@ class Work:
         # weak scaling (N > 1): every rank owns a full config-sized row block of an N-times taller
         # problem (its rows drawn with seed + 1000 * rank); strong: the config itself split by rows
         self.weak = scaling == "weak" and world > 1
-        rs = seed + 1000 * rank if self.weak else seed
+        from paper_2206_02874_b200.dist import shard_plan
+        self._plan = lambda M: shard_plan(M, world, rank, "weak" if self.weak else "strong", seed)
+        rs = self._plan(0)[2]                        # this rank's row seed
         g = tcxgen
         if cfg in ("c3", "c3tf32"):
             M = N = K = 8192
@@ -266,10 +268,8 @@ class Work:
             raise ValueError(cfg)
 
     def _rows(self, M):
-        if self.weak:
-            return 0, M
-        from paper_2206_02874_b200.dist import row_shard
-        return row_shard(M, self.world, self.rank)
+        m0, m1, _, _ = self._plan(M)
+        return m0, m1
 
     def _bcast(self, make):
         import torch.distributed as dist

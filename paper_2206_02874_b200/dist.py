@@ -28,6 +28,20 @@ def row_shard(M: int, world: int, rank: int, align: int = ROW_ALIGN):
     return min(M, b0 * align), min(M, b1 * align)
 
 
+def shard_plan(M: int, world: int, rank: int, scaling: str = "strong", seed: int = 0):
+    """(m0, m1, row_seed, M_total) for this rank.  strong: the M-row problem split by rows
+    (row_shard), rows drawn from the one seeded matrix; weak: every rank owns a full M-row block of a
+    world*M-row problem, its rows drawn with seed + 1000*rank (bench.py's default at N > 1)."""
+    if scaling not in ("strong", "weak"):
+        raise ValueError("scaling must be 'strong' or 'weak'")
+    if scaling == "weak" and world > 1:
+        if not 0 <= rank < world:
+            raise ValueError("bad world/rank")
+        return 0, M, seed + 1000 * rank, M * world
+    m0, m1 = row_shard(M, world, rank)
+    return m0, m1, seed, M
+
+
 def broadcast_replicated(t: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
     """the one data-path collective: replicate B from `src` to every rank (NCCL over NVLink)."""
     if dist.is_initialized() and dist.get_world_size(group) > 1:

@@ -74,3 +74,21 @@ def test_gloo_world2_broadcast_shard_gather():
         p.join(timeout=30)
     assert all(ok for _, ok, _ in res)
     assert all(t == 2.0 for _, _, t in res)       # max over ranks
+
+
+def test_shard_plan_weak_and_strong():
+    """bench.py's two multi-GPU modes: strong splits the config's rows (row_shard, one seed); weak
+    gives every rank a full config-sized block of a world-times taller problem with its own row seed,
+    so per-GPU work is fixed and no two ranks hold the same rows."""
+    for M in (8192, 16384, 65536):
+        for world in (1, 2, 4, 8):
+            strong = [tdist.shard_plan(M, world, r, "strong") for r in range(world)]
+            assert sum(m1 - m0 for m0, m1, _, _ in strong) == M
+            assert all(seed == 0 and total == M for _, _, seed, total in strong)
+            weak = [tdist.shard_plan(M, world, r, "weak") for r in range(world)]
+            assert all((m0, m1) == (0, M) for m0, m1, _, _ in weak)
+            assert all(total == M * world for *_, total in weak)
+            seeds = [seed for _, _, seed, _ in weak]
+            assert len(set(seeds)) == world and (world > 1 or seeds == [0])
+    with pytest.raises(ValueError):
+        tdist.shard_plan(256, 2, 0, "diagonal")
