@@ -106,12 +106,18 @@ def _check(st):
 
 
 def _ptr(t):
-    return None if t is None else ctypes.c_void_p(t.data_ptr())
+    return None if t is None else t.data_ptr()          # argtypes are c_void_p: plain ints marshal directly
+
+
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 
 
 def _stream(t=None):
-    dev = t.device if t is not None else torch.device("cuda")
-    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    """the caller's current stream on t's device, as the void* the C ABI takes"""
+    dev = t.device if t is not None else torch.device("cuda", torch.cuda.current_device())
+    if _raw_stream is not None:
+        return _raw_stream(dev.index if dev.index is not None else torch.cuda.current_device())
+    return torch.cuda.current_stream(dev).cuda_stream
 
 
 def launch_count() -> int:
@@ -187,10 +193,14 @@ def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, t
         raise ValueError("f16_acc: C must be float16")
     if D is None:
         D = torch.empty((M, N), dtype={S32: torch.int32, F16: torch.float16, F32: torch.float32}[cd], device=A.device)
+    ldc = C.stride(0) if C is not None else N
+    if not (cta_group or max_ctas or group_m or tile_n or pairs[0] or pairs[1] or _fault):
+        _check(lib().tcx_gemm(ab, cd, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(C), ldc, _ptr(D),
+                              D.stride(0), _stream(A)))
+        return D
     opts = GemmOpts(cta_group, max_ctas, group_m, tile_n, pairs[0], pairs[1], (ctypes.c_int * 2)(_fault, 0))
     _check(lib().tcx_gemm_ex(ab, cd, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
-                             _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
-                             ctypes.byref(opts), _stream(A)))
+                             _ptr(C), ldc, _ptr(D), D.stride(0), ctypes.byref(opts), _stream(A)))
     return D
 
 

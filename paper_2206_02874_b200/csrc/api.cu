@@ -2,6 +2,7 @@
 // Declarations and contracts: include/tcx.h.
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include "tcx_internal.h"
 
 namespace tcx {
@@ -41,6 +42,23 @@ tcx_status current_device(DevInfo* out) {
   if (out->cc_major != 10 || out->cc_minor != 0)
     return set_error(TCX_ERR_ARCH, "device %d is sm_%d%d; libtcx is built for sm_100a only", dev, out->cc_major, out->cc_minor);
   return TCX_OK;
+}
+
+cudaError_t ensure_max_smem(const void* kern, int bytes, int device) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, uint64_t> done;       // kernel -> bitmask of devices
+  const uint64_t bit = 1ull << (device & 63);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find(kern);
+    if (it != done.end() && (it->second & bit)) return cudaSuccess;
+  }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(mu);
+    done[kern] |= bit;
+  }
+  return e;
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

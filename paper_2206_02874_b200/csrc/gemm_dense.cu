@@ -82,6 +82,7 @@ struct Smem {
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];      // NH = 1: per buffer; NH = 2: per N-half of the single buffer
   uint64_t cbar[EPI_WARPS][2]; // epilogue: C chunk landed in staging buffer b of warp e
+  uint64_t cring[EPI_WARPS];   // epilogue, last tile: all of warp e's C chunks landed in the idle ring
   uint32_t tmem_base;
 };
 
@@ -150,7 +151,9 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   if (threadIdx.x == 0) {
     for (int s = 0; s < C_::STAGES; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], mc ? P : 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&sm->tmem_full[a], 1); mbar_init(&sm->tmem_empty[a], EPI_WARPS * CG); }
-    for (int w = 0; w < EPI_WARPS; ++w) { mbar_init(&sm->cbar[w][0], 1); mbar_init(&sm->cbar[w][1], 1); }
+    for (int w = 0; w < EPI_WARPS; ++w) {
+      mbar_init(&sm->cbar[w][0], 1); mbar_init(&sm->cbar[w][1], 1); mbar_init(&sm->cring[w], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 0 && elect_one()) { tma_prefetch(&tmA); tma_prefetch(&tmB); tma_prefetch(&tmC); tma_prefetch(&tmD); }
@@ -415,6 +418,12 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), lead_rank) : smem_u32(&sm->tmem_empty[0]);
     const int64_t my_tiles = cluster_id < num_tiles ? (num_tiles - 1 - cluster_id) / num_clusters + 1 : 0;
     const int64_t nq = my_tiles * CH;
+    // The CTA's last tile: once its accumulator is full every MMA has finished reading the operand
+    // ring and no load will refill it, so the epilogue stages the whole tile there (warp e: CH
+    // chunks of 4 KiB) — all C chunks are loaded at once and no chunk waits for an earlier store to
+    // free its buffer.  The exposed tail of every launch (and all of a one-tile problem) shrinks.
+    constexpr bool RING_LAST = NH == 1 && P == 1 && EPI_WARPS * CH * 4096 <= C_::SMEM_DATA;
+    const int64_t q_last0 = (my_tiles - 1) * CH;             // first chunk of the last tile
     auto coords = [&](int64_t q, int& x, int& y) {
       const int64_t it = q / CH;
       int64_t mt, nt;
@@ -423,16 +432,17 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       x = (int)(nt * C_::TILE_N + (q % CH) * 32);
     };
     auto load_c = [&](int64_t q) {
-      if (has_c && lane == 0 && q < nq) {
+      if (has_c && lane == 0 && q < nq && !(RING_LAST && q >= q_last0)) {
         int x, y; coords(q, x, y);
         mbar_arrive_expect_tx(&cbar[q & 1], 4096);
         tma_load_2d(stg + (q & 1) * 4096, &tmC, &cbar[q & 1], x, y);
       }
     };
     // single-buffered (wide) tiles: the epilogue is on the critical path, so each tile's C is
-    // L2-prefetched a tile ahead and its chunk loads hit L2 (double-buffered tiles hide the latency)
+    // L2-prefetched a tile ahead and its chunk loads hit L2 (double-buffered tiles hide the latency
+    // — except the first tile's, prefetched while the mainloop starts: small problems are one tile)
     auto prefetch_c_tile = [&](int64_t it) {
-      if (NH == 2 && has_c && lane == 0 && it < my_tiles)
+      if ((NH == 2 || it == 0) && has_c && lane == 0 && it < my_tiles)
         for (int ch = 0; ch < CH; ++ch) { int x, y; coords(it * CH + ch, x, y); tma_prefetch_2d(&tmC, x, y); }
     };
     prefetch_c_tile(0);
@@ -444,8 +454,21 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       prefetch_c_tile(it + 1);
       mbar_wait(&sm->tmem_full[acc], acc_phase);
       tc05_fence_after();
+      const bool ring = RING_LAST && it == my_tiles - 1;
+      uint8_t* const ring_stg = smem + e * CH * 4096;
+      if (ring && has_c) {                        // every C chunk of the tile, into the idle ring
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&sm->cring[e], CH * 4096);
+          for (int ch = 0; ch < CH; ++ch) {
+            int x, y; coords(it * CH + ch, x, y);
+            tma_load_2d(ring_stg + ch * 4096, &tmC, &sm->cring[e], x, y);
+          }
+        }
+        __syncwarp();
+      }
       uint32_t v[32], vn[32];
       tmem_ld_32x32b_x32(tmem_base + acc * NH * BN + lane_off, vn);   // chunk 0
+      if (ring && has_c) mbar_wait(&sm->cring[e], 0);
 #pragma unroll 1
       for (int ch = 0; ch < CH; ++ch) {
         const int64_t q = it * CH + ch;
@@ -458,7 +481,9 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           const int hn = (ch + 1) / (BN / 32);
           tmem_ld_32x32b_x32(tmem_base + (acc * NH + hn) * BN + ((ch + 1) % (BN / 32)) * 32 + lane_off, vn);
         }
-        if (has_c) {
+        if (ring) {
+          // own buffer per chunk in the ring; C (if any) already landed
+        } else if (has_c) {
           mbar_wait(&cbar[b], (cph >> b) & 1u);
           cph ^= 1u << b;
         } else if (q >= 2) {
@@ -472,7 +497,8 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(tmem_empty_cluster + (NH == 2 ? h : acc) * 8);
         }
-        uint8_t* rowp = stg + b * 4096 + lane * 128;          // this thread's row of the box
+        uint8_t* const buf = ring ? ring_stg + ch * 4096 : stg + b * 4096;
+        uint8_t* rowp = buf + lane * 128;                      // this thread's row of the box
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           uint4* p = (uint4*)(rowp + ((j ^ (lane & 7)) * 16)); // SW128: chunk j at j ^ (row % 8)
@@ -494,11 +520,12 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         __syncwarp();
         if (lane == 0) {
           int x, y; coords(q, x, y);
-          tma_store_2d(&tmD, stg + b * 4096, x, y);
+          tma_store_2d(&tmD, buf, x, y);
           bulk_commit();
-          if (has_c && q + 2 < nq) bulk_wait_read<0>();      // buffer b is free again ...
+          if (!ring && has_c && q + 2 < nq && !(RING_LAST && q + 2 >= q_last0))
+            bulk_wait_read<0>();                              // buffer b is free again ...
         }
-        load_c(q + 2);                                        // ... for the C chunk two ahead
+        if (!ring) load_c(q + 2);                             // ... for the C chunk two ahead
       }
 #if TCX_WATCHDOG
       if (trace && e == 0 && lane == 0 && rank == 0) {
@@ -554,7 +581,7 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
     tC = tD;                                                  // unused (has_c = 0)
   }
   auto kern = gemm_dense_kernel<CG, KIND, NH, PM, PN>;
-  TCX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_TOTAL));
+  TCX_CUDA_TRY(ensure_max_smem((const void*)kern, C_::SMEM_TOTAL, dev.device));
   const int64_t m_tiles = (a.M + C_::TILE_M - 1) / C_::TILE_M;
   const int64_t n_tiles = (a.N + C_::TILE_N - 1) / C_::TILE_N;
   int64_t clusters = ((m_tiles + PM - 1) / PM) * ((n_tiles + PN - 1) / PN);

@@ -454,7 +454,7 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
     tC = tD;
   }
   auto kern = gemm_sp24_kernel<CG, KIND, MW, PM, PN>;
-  TCX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_TOTAL));
+  TCX_CUDA_TRY(ensure_max_smem((const void*)kern, C_::SMEM_TOTAL, dev.device));
   const int64_t m_tiles = a.M / C_::TILE_M, n_tiles = (a.N + BN - 1) / BN;
   int64_t clusters = ((m_tiles + PM - 1) / PM) * ((n_tiles + PN - 1) / PN);
   int64_t max_clusters = dev.sm_count / CL;

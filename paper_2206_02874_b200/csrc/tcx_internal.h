@@ -17,7 +17,9 @@ tcx_status set_error(tcx_status s, const char* fmt, ...);
 inline tcx_status ok() { return TCX_OK; }
 
 struct DevInfo { int device; int sm_count; int cc_major; int cc_minor; int max_smem_optin; };
-tcx_status current_device(DevInfo* out);   // validates sm_100
+tcx_status current_device(DevInfo* out);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device), not per launch
+cudaError_t ensure_max_smem(const void* kern, int bytes, int device);   // validates sm_100
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed)
 tcx_status make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base,
