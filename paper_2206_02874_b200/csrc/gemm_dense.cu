@@ -324,11 +324,22 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), lead_rank) : smem_u32(&sm->tmem_empty[0]);
     const int64_t my_tiles = cluster_id < num_tiles ? (num_tiles - 1 - cluster_id) / num_clusters + 1 : 0;
     const uint32_t lane_off = (uint32_t)(e * 32) << 16;
-    auto coords = [&](int64_t it, int ch, int& x, int& y) {
+    // origins of the (at most two) tiles the epilogue addresses at a time — this one and the next —
+    // cached, so the raster's 64-bit divisions (~800 cycles) run once per tile, not once per chunk
+    int64_t oa_it = -1, ob_it = -1;
+    int oa_x = 0, oa_y = 0, ob_x = 0, ob_y = 0;
+    auto origin = [&](int64_t it, int& x, int& y) {
+      if (it == oa_it) { x = oa_x; y = oa_y; return; }
+      if (it == ob_it) { x = ob_x; y = ob_y; return; }
       int64_t mt, nt;
       pair_tile(cluster_id + it * num_clusters, mt, nt);
+      x = (int)(nt * C_::TILE_N);
       y = (int)(mt * C_::TILE_M + rank * BM + e * 32);
-      x = (int)(nt * C_::TILE_N + ch * 32);
+      if (oa_it < ob_it) { oa_it = it; oa_x = x; oa_y = y; } else { ob_it = it; ob_x = x; ob_y = y; }
+    };
+    auto coords = [&](int64_t it, int ch, int& x, int& y) {
+      origin(it, x, y);
+      x += ch * 32;
     };
     auto preload_c = [&](int64_t it, int buf) {
       if (lane == 0) bulk_wait_read<0>();       // staging no longer read by earlier D stores
@@ -424,12 +435,22 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     // free its buffer.  The exposed tail of every launch (and all of a one-tile problem) shrinks.
     constexpr bool RING_LAST = NH == 1 && P == 1 && EPI_WARPS * CH * 4096 <= C_::SMEM_DATA;
     const int64_t q_last0 = (my_tiles - 1) * CH;             // first chunk of the last tile
-    auto coords = [&](int64_t q, int& x, int& y) {
-      const int64_t it = q / CH;
+    // origins of the (at most two) tiles the epilogue addresses at a time — this one and the next —
+    // cached, so the raster's 64-bit divisions (~800 cycles) run once per tile, not once per chunk
+    int64_t oa_it = -1, ob_it = -1;
+    int oa_x = 0, oa_y = 0, ob_x = 0, ob_y = 0;
+    auto origin = [&](int64_t it, int& x, int& y) {
+      if (it == oa_it) { x = oa_x; y = oa_y; return; }
+      if (it == ob_it) { x = ob_x; y = ob_y; return; }
       int64_t mt, nt;
       pair_tile(cluster_id + it * num_clusters, mt, nt);
+      x = (int)(nt * C_::TILE_N);
       y = (int)(mt * C_::TILE_M + rank * BM + e * 32);
-      x = (int)(nt * C_::TILE_N + (q % CH) * 32);
+      if (oa_it < ob_it) { oa_it = it; oa_x = x; oa_y = y; } else { ob_it = it; ob_x = x; ob_y = y; }
+    };
+    auto coords = [&](int64_t q, int& x, int& y) {
+      origin(q / CH, x, y);
+      x += (int)(q % CH) * 32;
     };
     auto load_c = [&](int64_t q) {
       if (has_c && lane == 0 && q < nq && !(RING_LAST && q >= q_last0)) {

@@ -323,12 +323,24 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), lead_rank) : smem_u32(&sm->tmem_empty[0]);
     const int64_t my_tiles = cluster_id < num_tiles ? (num_tiles - 1 - cluster_id) / num_clusters + 1 : 0;
     const int64_t nq = my_tiles * CH;
-    auto coords = [&](int64_t q, int& x, int& y) {
+    // origins of the (at most two) tiles the epilogue addresses at a time — this one and the next —
+    // cached, so the raster's 64-bit divisions (~800 cycles) run once per tile, not once per chunk
+    int64_t oa_it = -1, ob_it = -1;
+    int oa_x = 0, oa_y = 0, ob_x = 0, ob_y = 0;
+    auto origin = [&](int64_t it, int& x, int& y) {
+      if (it == oa_it) { x = oa_x; y = oa_y; return; }
+      if (it == ob_it) { x = ob_x; y = ob_y; return; }
       int64_t mt, nt;
-      pair_tile(cluster_id + (q / CH) * num_clusters, mt, nt);
+      pair_tile(cluster_id + it * num_clusters, mt, nt);
+      x = (int)(nt * BN);
+      y = (int)(mt * C_::TILE_M + rank * BM + e * 32);
+      if (oa_it < ob_it) { oa_it = it; oa_x = x; oa_y = y; } else { ob_it = it; ob_x = x; ob_y = y; }
+    };
+    auto coords = [&](int64_t q, int& x, int& y) {
+      origin(q / CH, x, y);
       const int ch = (int)(q % CH);
-      y = (int)(mt * C_::TILE_M + (ch / HCH) * BM * CG + rank * BM + e * 32);
-      x = (int)(nt * BN + (ch % HCH) * 16);
+      y += (ch / HCH) * BM * CG;
+      x += (ch % HCH) * 16;
     };
     auto load_c = [&](int64_t q) {
       if (has_c && lane == 0 && q < nq) {
