@@ -99,9 +99,10 @@ typedef struct {
   int max_ctas;    /* cap on persistent CTAs (0 = all SMs) */
   int group_m;     /* tile raster (0 = default): > 0, that many cluster-tile rows sweep N together;
                       < 0, |group_m| cluster-tile columns sweep M together */
-  int tile_n;      /* 0 = library choice; 512: tcx_gemm's 256 x 512 pair tile (two N = 256 MMAs
-                      share A), tcx_gemm_sp24's 512 x 240 pair tile (two M-halves share B;
-                      F16/BF16/TF32, M % 512 == 0) */
+  int tile_n;      /* 0 = library choice; tcx_gemm: 256 (default) or 512 = the 256 x 512 pair tile
+                      (two N = 256 MMAs share A); tcx_gemm_sp24 (the tile HEIGHT): 512 = the
+                      512 x 240 pair tile (two M-halves share B; F16/BF16/TF32, M % 512 == 0 — the
+                      default there), 256 = the 256 x 240 tile (the default otherwise) */
   int pairs_m;     /* CTA pair only (not with tile_n = 512): groups of pairs_m x pairs_n CTA pairs   */
   int pairs_n;     /* compute adjacent pair tiles and are launched as preferred clusters; where the  */
                    /* hardware forms the cluster, A (sA) is TMA-multicast across the pairs_n pairs  */

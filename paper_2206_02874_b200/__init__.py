@@ -260,7 +260,7 @@ def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m
     cd = S32 if ab == S8 else F32
     if D is None:
         D = torch.empty((M, N), dtype=torch.int32 if cd == S32 else torch.float32, device=vals.device)
-    opts = GemmOpts(cta_group, max_ctas, group_m, 512 if tile_m == 512 else 0, pairs[0], pairs[1])
+    opts = GemmOpts(cta_group, max_ctas, group_m, int(tile_m), pairs[0], pairs[1])
     _check(lib().tcx_gemm_sp24_ex(ab, cd, M, N, K, _ptr(vals), vals.stride(0), _ptr(meta_hw), _ptr(B), B.stride(0),
                                   _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
                                   ctypes.byref(opts), _stream(vals)))

@@ -334,6 +334,8 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
     if (opts->cta_group == 1 || opts->cta_group == 2) g.cta_group = opts->cta_group;
     g.max_ctas = opts->max_ctas;
     g.group_m = opts->group_m;
+    if (opts->tile_n != 0 && opts->tile_n != 256 && opts->tile_n != 512)
+      return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm_sp24: tile_n (tile height) must be 0, 256 or 512");
     g.tile_n = opts->tile_n;
     const int pm = opts->pairs_m ? opts->pairs_m : 1, pn = opts->pairs_n ? opts->pairs_n : 1;
     if (pm < 1 || pm > 2 || pn < 1 || pn > 2)

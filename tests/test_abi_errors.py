@@ -77,6 +77,7 @@ def _sp(ab=F16, cd=F32, M=256, N=240, K=256, meta=P, opts=None):
     (dict(M=128), UNSUPPORTED),                      # the CTA pair needs M % 256
     (dict(ab=S8, cd=F32, K=256), UNSUPPORTED),
     (dict(opts=_opts(pairs_m=2, tile_n=512)), INVALID),
+    (dict(opts=_opts(tile_n=384)), INVALID),
     (dict(M=0), OK),
 ])
 def test_sparse_argument_errors(kw, want):

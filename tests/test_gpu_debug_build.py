@@ -149,7 +149,7 @@ for tm in (0, 512):
     T = (M // (512 if tm else 256)) * (N // 240)
     buf = torch.zeros(4 * T, dtype=torch.int64, device=dev)
     tcx.debug_trace(buf)
-    tcx.gemm_sp24(vals, hw, B, None, tile_m=tm, max_ctas=4)
+    tcx.gemm_sp24(vals, hw, B, None, tile_m=tm or 256, max_ctas=4)
     torch.cuda.synchronize()
     tcx.debug_trace(None)
     out[str(tm)] = buf.view(T, 4).cpu().numpy()

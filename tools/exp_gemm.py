@@ -49,7 +49,7 @@ def main():
         kw = parse(v)
         wide = kw.pop("wide", False)
         if cfg == "c5":
-            step = lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, tile_m=512 if wide else 0, **kw)
+            step = lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, tile_m=512 if wide else 256, **kw)
         else:
             step = lambda: tcx.gemm(w.A, w.B, w.C, w.D, tf32=getattr(w, "tf32", False), tile_n=512 if wide else 0, **kw)
         for _ in range(3):

@@ -41,7 +41,7 @@ def main():
     M, N, K = w.shape
     if cfg.startswith("c5"):
         m_tiles, n_tiles = M // (512 if wide else 256), (N + 239) // 240
-        step = lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, group_m=g, tile_m=512 if wide else 0)
+        step = lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, group_m=g, tile_m=512 if wide else 256)
     else:
         tn = 512 if wide else 256                            # dense: the 256 x 512 pair tile
         m_tiles, n_tiles = (M + 255) // 256, (N + tn - 1) // tn
