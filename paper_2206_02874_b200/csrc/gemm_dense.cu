@@ -520,12 +520,17 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         }
         uint8_t* const buf = ring ? ring_stg + ch * 4096 : stg + b * 4096;
         uint8_t* rowp = buf + lane * 128;                      // this thread's row of the box
+        uint4 cv[8];                                           // all C loads first: 8 in flight
+        if (has_c) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) cv[j] = *(const uint4*)(rowp + ((j ^ (lane & 7)) * 16));
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           uint4* p = (uint4*)(rowp + ((j ^ (lane & 7)) * 16)); // SW128: chunk j at j ^ (row % 8)
           uint4 o = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           if (has_c) {
-            const uint4 c = *p;
+            const uint4 c = cv[j];
             if constexpr (KIND == KIND_I8) {                   // S32: wrap mod 2^32
               o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
             } else {                                          // FP32: one RNE add

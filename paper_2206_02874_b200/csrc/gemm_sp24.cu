@@ -390,12 +390,17 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           __syncwarp();
         }
         uint8_t* rowp = stg + b * 2048 + lane * 64;            // this thread's row of the box
+        uint4 cv[4];                                           // all C loads first: 4 in flight
+        if (has_c) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cv[j] = *(const uint4*)(rowp + ((j ^ ((lane >> 1) & 3)) * 16));
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           uint4* p = (uint4*)(rowp + ((j ^ ((lane >> 1) & 3)) * 16));   // SW64: chunk j at j ^ ((row/2) % 4)
           uint4 o = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           if (has_c) {
-            const uint4 c = *p;
+            const uint4 c = cv[j];
             if constexpr (KIND == KIND_I8) {                   // S32: wrap mod 2^32
               o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
             } else {                                          // FP32: one RNE add
