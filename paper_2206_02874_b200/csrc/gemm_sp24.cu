@@ -28,6 +28,10 @@ constexpr int BN = 240;            // UMMA N
 constexpr int NUM_THREADS = 256;
 constexpr int EPI_WARPS = 4;
 constexpr int GROUP_M = 8;            // default raster group (cluster-tile rows sweeping N together)
+// epilogue staging buffers per warp: the C chunk two ahead goes into the buffer the store before
+// last read, so issuing it waits only for that older store, not for the one just issued
+constexpr int STG_BUFS = 3;
+constexpr int C_AHEAD = 2;
 // MW = 1 ("M-wide", CTA pair tile 512 x 240): two M-halves share each stage's B (30 of the 48 KiB a
 // stage moves), so a stage carries 66 KiB for twice the work — 31% fewer operand bytes per FLOP
 // into each SM, whose TMA ingress the 2:4 stream otherwise saturates.  Both halves'
@@ -58,7 +62,7 @@ struct SpCfg {
   static constexpr int STAGES = CG == 1 ? 2 : (MW ? 3 : 4);
   static constexpr int TILE_M = BM * CG * MH;
   static constexpr int SMEM_DATA = STAGES * STAGE_BYTES;
-  static constexpr int STG_BYTES = EPI_WARPS * 2 * 2048;   // epilogue: 2 x 2 KiB (32 rows x 16 cols) per warp
+  static constexpr int STG_BYTES = EPI_WARPS * STG_BUFS * 2048;   // epilogue: 3 x 2 KiB (32 rows x 16 cols) per warp
   static constexpr int SMEM_TOTAL = SMEM_DATA + STG_BYTES + 1024 + 1024;
   static constexpr int META_COL = 512 - STAGES * META_COLS;    // metadata ring at the top of TMEM
   // accumulator columns: MW -> M-half h at h * BN (one buffer); else buffer b at b * ACC_STRIDE
@@ -74,7 +78,7 @@ struct Smem {
   uint64_t empty[8];
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
-  uint64_t cbar[EPI_WARPS][2]; // epilogue: C chunk landed in staging buffer b of warp e
+  uint64_t cbar[EPI_WARPS][STG_BUFS]; // epilogue: C chunk landed in staging buffer b of warp e
   uint32_t tmem_base;
 };
 
@@ -143,7 +147,8 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (threadIdx.x == 0) {
     for (int s = 0; s < C_::STAGES; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], mc ? P : 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&sm->tmem_full[a], 1); mbar_init(&sm->tmem_empty[a], EPI_WARPS * CG); }
-    for (int w = 0; w < EPI_WARPS; ++w) { mbar_init(&sm->cbar[w][0], 1); mbar_init(&sm->cbar[w][1], 1); }
+    for (int w = 0; w < EPI_WARPS; ++w)
+      for (int b = 0; b < STG_BUFS; ++b) mbar_init(&sm->cbar[w][b], 1);
     fence_mbar_init();
   }
   if (warp == 0 && elect_one()) { tma_prefetch(&tmA); tma_prefetch(&tmB); tma_prefetch(&tmE); tma_prefetch(&tmC); tma_prefetch(&tmD); }
@@ -317,7 +322,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const int lane = threadIdx.x & 31;
     constexpr int HCH = BN / 16;                 // chunks per accumulator (M-half)
     constexpr int CH = HCH * MH;                 // chunks per tile
-    uint8_t* stg = smem + C_::SMEM_DATA + e * 4096;
+    uint8_t* stg = smem + C_::SMEM_DATA + e * STG_BUFS * 2048;
     uint64_t* cbar = &sm->cbar[e][0];
     uint32_t cph = 0u;                            // bit b: phase of cbar[b] (a register, not a local array)
     const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), lead_rank) : smem_u32(&sm->tmem_empty[0]);
@@ -345,8 +350,9 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     auto load_c = [&](int64_t q) {
       if (has_c && lane == 0 && q < nq) {
         int x, y; coords(q, x, y);
-        mbar_arrive_expect_tx(&cbar[q & 1], 2048);
-        tma_load_2d(stg + (q & 1) * 2048, &tmC, &cbar[q & 1], x, y);
+        const int bq = (int)(q % STG_BUFS);
+        mbar_arrive_expect_tx(&cbar[bq], 2048);
+        tma_load_2d(stg + bq * 2048, &tmC, &cbar[bq], x, y);
       }
     };
     // single-buffered (wide) tiles: the epilogue is on the critical path, so each tile's C is
@@ -371,7 +377,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll 1
       for (int ch = 0; ch < CH; ++ch) {
         const int64_t q = it * CH + ch;
-        const int b = (int)(q & 1);
+        const int b = (int)(q % STG_BUFS);
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = vn[j];
@@ -385,8 +391,8 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if (has_c) {
           mbar_wait(&cbar[b], (cph >> b) & 1u);
           cph ^= 1u << b;
-        } else if (q >= 2) {
-          if (lane == 0) bulk_wait_read<1>();     // the store of chunk q-2 has read buffer b
+        } else if (q >= STG_BUFS) {
+          if (lane == 0) bulk_wait_read<STG_BUFS - 1>();   // the store of chunk q - STG_BUFS has read buffer b
           __syncwarp();
         }
         uint8_t* rowp = stg + b * 2048 + lane * 64;            // this thread's row of the box
@@ -418,9 +424,10 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           int x, y; coords(q, x, y);
           tma_store_2d(&tmD, stg + b * 2048, x, y);
           bulk_commit();
-          if (has_c && q + 2 < nq) bulk_wait_read<0>();
+          // the buffer of chunk q + C_AHEAD was last read by the store of chunk q + C_AHEAD - STG_BUFS
+          if (has_c && q + C_AHEAD < nq) bulk_wait_read<STG_BUFS - C_AHEAD>();
         }
-        load_c(q + 2);
+        load_c(q + C_AHEAD);
       }
 #if TCX_WATCHDOG
       if (trace && e == 0 && lane == 0 && rank == 0) {
