@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/gputests.log 2>&1; echo tests=$?
+timeout 900 python bench.py > gpurun_out/bench_k.json 2> gpurun_out/bench_k.err; echo bench=$?
+bash tools/gpu/profile.sh r01f
