@@ -102,7 +102,8 @@ typedef struct {
   int tile_n;      /* 0 = library choice; tcx_gemm: 256 (default) or 512 = the 256 x 512 pair tile
                       (two N = 256 MMAs share A); tcx_gemm_sp24 (the tile HEIGHT): 512 = the
                       512 x 240 pair tile (two M-halves share B; F16/BF16/TF32, M % 512 == 0 — the
-                      default there), 256 = the 256 x 240 tile (the default otherwise) */
+                      default there when M*N*K >= 2^43, i.e. calls long enough to run at the
+                      power cap), 256 = the 256 x 240 tile (the default otherwise) */
   int pairs_m;     /* CTA pair only (not with tile_n = 512): groups of pairs_m x pairs_n CTA pairs   */
   int pairs_n;     /* compute adjacent pair tiles and are launched as preferred clusters; where the  */
                    /* hardware forms the cluster, A (sA) is TMA-multicast across the pairs_n pairs  */

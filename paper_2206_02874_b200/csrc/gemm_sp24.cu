@@ -513,13 +513,16 @@ template <int KIND>
 tcx_status launch_sp_kind(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   if (a.cta_group == 1) return launch_sp<1, KIND>(a, dev, s);
   // tile_m = 512 (opts.tile_n field reused as the sparse tile height): the M-wide pair tile
-  // the 512 x 240 M-wide tile is the default where it applies (F16/BF16/TF32, M % 512 == 0, no
-  // multicast group): since the epilogue stopped recomputing tile origins per chunk, its shorter
-  // single-buffer drain costs less than its 31% fewer operand bytes save under the power cap (C5 +5%,
-  // profiles/r01_wide_tile_study.txt); tile_n = 256 forces the 256 x 240 tile
+  // the 512 x 240 M-wide tile is the default for long calls (F16/BF16/TF32, M % 512 == 0, no
+  // multicast group, M*N*K >= 2^43 — a call of >= ~10 ms, which runs at the board's power cap): there
+  // its 31% fewer operand bytes per FLOP are worth more than its single-buffer drain (C5 +5.3%); on
+  // shorter calls the clock is not yet power-capped and the double-buffered 256 x 240 tile wins by
+  // 10-25% (profiles/r01_wide_tile_study.txt).  tile_n = 256 / 512 forces either.
   if constexpr (KIND != KIND_I8) {
     const bool grouped = a.pairs_m > 1 || a.pairs_n > 1;
-    if (a.M % 512 == 0 && (a.tile_n == 512 || (a.tile_n == 0 && !grouped))) return launch_sp<2, KIND, 1>(a, dev, s);
+    const bool long_call = (double)a.M * (double)a.N * (double)a.K >= 8796093022208.0;   // 2^43
+    if (a.M % 512 == 0 && (a.tile_n == 512 || (a.tile_n == 0 && !grouped && long_call)))
+      return launch_sp<2, KIND, 1>(a, dev, s);
   }
   if (a.pairs_m == 2 && a.pairs_n == 2) return launch_sp<2, KIND, 0, 2, 2>(a, dev, s);
   if (a.pairs_m == 2) return launch_sp<2, KIND, 0, 2, 1>(a, dev, s);
