@@ -316,8 +316,8 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   } else if (warp >= 4) {
     // per 16-column chunk: tcgen05.ld (thread = row) -> (+ C chunk TMA-loaded into a 64B-swizzled
     // 2 KiB staging buffer) -> result back into the buffer -> one TMA store of the 32 x 16 box
-    // (coalesced full-line HBM writes, TMA clips rows >= M / columns >= N).  Two buffers per warp
-    // alternate, the C chunk two ahead loading while this one is stored (as in gemm_dense.cu).
+    // (coalesced full-line HBM writes, TMA clips rows >= M / columns >= N).  STG_BUFS buffers per
+    // warp rotate, the C chunk C_AHEAD ahead loading while this one is stored.
     const int e = warp - 4;
     const int lane = threadIdx.x & 31;
     constexpr int HCH = BN / 16;                 // chunks per accumulator (M-half)
