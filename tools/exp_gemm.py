@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Kernel-configuration sweep for the GEMM paths (raster group, CTA mode).
 
-usage: python tools/exp_gemm.py c5|c3|c4|c3tf32 [steps] [variant ...]
+usage: python tools/exp_gemm.py c5|c3|c4|c3tf32|c4sp|c3sptf32 [steps] [variant ...]
 variant = "g<group_m>c<cta_group>[w][p<pm><pn>]" e.g. g8c2, g16c2, g8c1, g8c2w (w = the 512-wide tile),
 g8c2p12 (multicast cluster of 1 x 2 CTA pairs).  Prints one JSON line per variant
 with device time (CUDA events), TFLOP/s, NVML SM clock / power during the run, and whether D is
@@ -48,8 +48,10 @@ def main():
     for v in variants:
         kw = parse(v)
         wide = kw.pop("wide", False)
-        if cfg == "c5":
-            step = lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, tile_m=512 if wide else 256, **kw)
+        if hasattr(w, "vals"):                          # sparse configs (c5, c4sp, c3sptf32)
+            tf = cfg == "c3sptf32"
+            step = lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, tf32=tf,
+                                         tile_m=512 if wide else 256, **kw)
         else:
             step = lambda: tcx.gemm(w.A, w.B, w.C, w.D, tf32=getattr(w, "tf32", False), tile_n=512 if wide else 0, **kw)
         for _ in range(3):
