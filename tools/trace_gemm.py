@@ -34,18 +34,19 @@ def tile_coords(t, m_tiles, n_tiles, g):
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
     g = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-    wide = len(sys.argv) > 3 and sys.argv[3] == "wide"      # c5: the 512 x 240 M-wide tile
+    wide = "wide" in sys.argv[3:]                            # c5: the 512 x 240 M-wide tile
+    noc = "noc" in sys.argv[3:]                              # D = A B (no C): the epilogue's C path off
     torch.cuda.set_device(0)
     w = bench.Work(cfg, 0, 1, torch.device("cuda", 0))
     tcx = w.tcx
     M, N, K = w.shape
     if cfg.startswith("c5"):
         m_tiles, n_tiles = M // (512 if wide else 256), (N + 239) // 240
-        step = lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, group_m=g, tile_m=512 if wide else 256)
+        step = lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, None if noc else w.C, w.D, group_m=g, tile_m=512 if wide else 256)
     else:
         tn = 512 if wide else 256                            # dense: the 256 x 512 pair tile
         m_tiles, n_tiles = (M + 255) // 256, (N + tn - 1) // tn
-        step = lambda: tcx.gemm(w.A, w.B, w.C, w.D, tf32=getattr(w, "tf32", False), group_m=g, tile_n=tn)
+        step = lambda: tcx.gemm(w.A, w.B, None if noc else w.C, w.D, tf32=getattr(w, "tf32", False), group_m=g, tile_n=tn)
     T = m_tiles * n_tiles
     buf = torch.zeros(4 * T, dtype=torch.int64, device="cuda")
     for _ in range(3):
@@ -93,6 +94,7 @@ def main():
     rep["inter_tile_mma_gap_us"] = {"median": float(np.median(gaps)), "p90": float(np.percentile(gaps, 90))} if gaps.size else None
     rep["mma_busy_fraction"] = float(dur.sum() / (dur.sum() + gaps.sum())) if gaps.size else None
     rep["wide"] = wide
+    rep["no_c"] = noc
     print(json.dumps(rep))
     np.save(os.path.join(os.environ.get("TCX_REPORT_DIR", "gpurun_out"), f"trace_{cfg}_g{g}{'_wide' if wide else ''}.npy"), r)
 
