@@ -358,11 +358,11 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         const int b = ch & 1;
         mbar_wait(&cbar[b], (cph >> b) & 1u);
         cph ^= 1u << b;
-        const uint8_t* rowp = stg + b * 2048 + lane * 64;
+        const uint32_t rowa = smem_u32(stg) + b * 2048 + lane * 64;
         uint32_t r[32];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint4 w = *(const uint4*)(rowp + ((j ^ ((lane >> 1) & 3)) * 16));   // SW64
+          const uint4 w = lds128(rowa + ((j ^ ((lane >> 1) & 3)) * 16));   // SW64
           const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
           for (int i = 0; i < 4; ++i) { r[8 * j + 2 * i] = ws[i] & 0xFFFFu; r[8 * j + 2 * i + 1] = ws[i] >> 16; }
@@ -392,12 +392,12 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         if (lane == 0 && nstore >= 2) bulk_wait_read<1>();   // store nstore-2 has read buffer b
         __syncwarp();
         tmem_ld_wait();
-        uint8_t* rowp = stg + b * 2048 + lane * 64;
+        const uint32_t rowa = smem_u32(stg) + b * 2048 + lane * 64;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint4 w = make_uint4((v[8 * j] & 0xFFFFu) | (v[8 * j + 1] << 16), (v[8 * j + 2] & 0xFFFFu) | (v[8 * j + 3] << 16),
                                      (v[8 * j + 4] & 0xFFFFu) | (v[8 * j + 5] << 16), (v[8 * j + 6] & 0xFFFFu) | (v[8 * j + 7] << 16));
-          *(uint4*)(rowp + ((j ^ ((lane >> 1) & 3)) * 16)) = w;
+          sts128(rowa + ((j ^ ((lane >> 1) & 3)) * 16), w);
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -471,9 +471,22 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     load_c(1);
     int acc = 0; uint32_t acc_phase = 0;
     const uint32_t lane_off = (uint32_t)(e * 32) << 16;
+#if TCX_WATCHDOG
+    // debug chunk-phase stamps (clock64): cluster 0, CTA rank 0, lane 0 of each epilogue warp e,
+    // first CHUNK_TILES tiles, 8 per chunk, after the tile timeline (trace_cap >= num_tiles + ...)
+    constexpr int CHUNK_TILES = 6;
+    uint64_t* const cst = (trace && cluster_id == 0 && rank == 0 && lane == 0 &&
+                           trace_cap >= num_tiles + 8 * CHUNK_TILES * CH)
+                              ? trace + 4 * num_tiles + e * CHUNK_TILES * CH * 8 : nullptr;
+#define TCX_STAMP(it_, ch_, k_) do { if (cst && (it_) < CHUNK_TILES) cst[((it_) * CH + (ch_)) * 8 + (k_)] = clock64(); } while (0)
+#else
+#define TCX_STAMP(it_, ch_, k_) do { } while (0)
+#endif
     for (int64_t it = 0; it < my_tiles; ++it) {
       prefetch_c_tile(it + 1);
+      TCX_STAMP(it, 0, 7);
       mbar_wait(&sm->tmem_full[acc], acc_phase);
+      TCX_STAMP(it, 1, 7);
       tc05_fence_after();
       const bool ring = RING_LAST && it == my_tiles - 1;
       uint8_t* const ring_stg = smem + e * CH * 4096;
@@ -495,7 +508,9 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         const int64_t q = it * CH + ch;
         const int b = (int)(q & 1);
         const int h = ch / (BN / 32);
+        TCX_STAMP(it, ch, 0);
         tmem_ld_wait();                           // chunk ch has landed in vn
+        TCX_STAMP(it, ch, 1);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = vn[j];
         if (ch + 1 < CH) {                        // read the next chunk while this one is stored
@@ -511,6 +526,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           if (lane == 0) bulk_wait_read<1>();     // the store of chunk q-2 has read buffer b
           __syncwarp();
         }
+        TCX_STAMP(it, ch, 2);
         if (ch % (BN / 32) == BN / 32 - 1 && (NH == 2 || ch == CH - 1)) {
           // this part of the accumulator is read: hand it back to the MMA warp
           // (NH = 1: the whole buffer `acc`; NH = 2: N-half h of the single buffer)
@@ -519,15 +535,15 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           if (lane == 0) mbar_arrive_cluster(tmem_empty_cluster + (NH == 2 ? h : acc) * 8);
         }
         uint8_t* const buf = ring ? ring_stg + ch * 4096 : stg + b * 4096;
-        uint8_t* rowp = buf + lane * 128;                      // this thread's row of the box
+        const uint32_t rowa = smem_u32(buf) + lane * 128;      // this thread's row of the box
         uint4 cv[8];                                           // all C loads first: 8 in flight
         if (has_c) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) cv[j] = *(const uint4*)(rowp + ((j ^ (lane & 7)) * 16));
+          for (int j = 0; j < 8; ++j) cv[j] = lds128(rowa + ((j ^ (lane & 7)) * 16));
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          uint4* p = (uint4*)(rowp + ((j ^ (lane & 7)) * 16)); // SW128: chunk j at j ^ (row % 8)
+          const uint32_t pa = rowa + ((j ^ (lane & 7)) * 16);  // SW128: chunk j at j ^ (row % 8)
           uint4 o = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           if (has_c) {
             const uint4 c = cv[j];
@@ -540,17 +556,21 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
               o.w = __float_as_uint(__fadd_rn(__uint_as_float(o.w), __uint_as_float(c.w)));
             }
           }
-          *p = o;
+          sts128(pa, o);
         }
+        TCX_STAMP(it, ch, 3);
         fence_proxy_async_smem();
         __syncwarp();
+        TCX_STAMP(it, ch, 4);
         if (lane == 0) {
           int x, y; coords(q, x, y);
           tma_store_2d(&tmD, buf, x, y);
           bulk_commit();
+          TCX_STAMP(it, ch, 5);
           if (!ring && has_c && q + 2 < nq && !(RING_LAST && q + 2 >= q_last0))
             bulk_wait_read<0>();                              // buffer b is free again ...
         }
+        TCX_STAMP(it, ch, 6);
         if (!ring) load_c(q + 2);                             // ... for the C chunk two ahead
       }
 #if TCX_WATCHDOG
@@ -562,6 +582,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       if (++acc == C_::NBUF) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) bulk_wait<0>();                            // stores complete before exit
+#undef TCX_STAMP
   }
 
   tc05_fence_before();

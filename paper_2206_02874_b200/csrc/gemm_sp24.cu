@@ -395,15 +395,15 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           if (lane == 0) bulk_wait_read<STG_BUFS - 1>();   // the store of chunk q - STG_BUFS has read buffer b
           __syncwarp();
         }
-        uint8_t* rowp = stg + b * 2048 + lane * 64;            // this thread's row of the box
+        const uint32_t rowa = smem_u32(stg) + b * 2048 + lane * 64;   // this thread's row of the box
         uint4 cv[4];                                           // all C loads first: 4 in flight
         if (has_c) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) cv[j] = *(const uint4*)(rowp + ((j ^ ((lane >> 1) & 3)) * 16));
+          for (int j = 0; j < 4; ++j) cv[j] = lds128(rowa + ((j ^ ((lane >> 1) & 3)) * 16));
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          uint4* p = (uint4*)(rowp + ((j ^ ((lane >> 1) & 3)) * 16));   // SW64: chunk j at j ^ ((row/2) % 4)
+          const uint32_t pa = rowa + ((j ^ ((lane >> 1) & 3)) * 16);   // SW64: chunk j at j ^ ((row/2) % 4)
           uint4 o = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           if (has_c) {
             const uint4 c = cv[j];
@@ -416,7 +416,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               o.w = __float_as_uint(__fadd_rn(__uint_as_float(o.w), __uint_as_float(c.w)));
             }
           }
-          *p = o;
+          sts128(pa, o);
         }
         fence_proxy_async_smem();
         __syncwarp();

@@ -13,6 +13,18 @@ namespace tcx {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// 16-byte shared-window accesses by 32-bit address: LDS.128 / STS.128.  A dereference of the
+// aligned extern-shared pointer compiles to generic LD/ST.E.128 (64-bit address arithmetic, the
+// generic-window check) because the alignment cast loses the address space.  volatile + memory
+// clobber keep them ordered with the mbarrier waits and proxy fences around them.
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 
 
 __device__ __forceinline__ bool elect_one() {
