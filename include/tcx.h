@@ -128,7 +128,12 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
  * 4 * capacity uint64 (caller-owned, NULL = off); tile record i (cluster tile i of the launch's raster):
  *   [0] = pair id << 32 | tile index, [1] = %globaltimer ns when the tile's first MMA issued,
  *   [2] = when its last MMA was committed, [3] = when the epilogue issued its last store.
- * Records past `capacity` are dropped.  Used to study L2 reuse across concurrent tiles. */
+ * Records past `capacity` are dropped.  Used to study L2 reuse across concurrent tiles.
+ * Dense kernel, 32-bit accumulate: if capacity >= T + 48 * CH (T = the launch's cluster tiles,
+ * CH = 32-column chunks per tile: 8, or 16 for tile_n 512), the records are followed by chunk-phase
+ * stamps (clock64 of cluster 0, CTA rank 0, lane 0 of epilogue warp e = 0..3, its first 6 tiles):
+ * uint64 index 4 T + ((e * 6 + tile) * CH + chunk) * 8 + k, k = 0..6 the epilogue's phases and
+ * k = 7 (chunks 0 / 1) before / after the accumulator-full wait (tools/chunk_trace.py reads them). */
 tcx_status tcx_debug_trace(void* d_buf, int64_t capacity);
 
 /* ---------------------------------------------------------------------------------------
