@@ -163,3 +163,36 @@ print("OK")
         t = z[k].astype(np.int64)
         assert np.array_equal(t[:, 0] & 0xFFFFFFFF, np.arange(len(t))), k
         assert np.all(t[:, 1] > 0) and np.all(t[:, 1] <= t[:, 2]) and np.all(t[:, 2] <= t[:, 3]), k
+
+
+def test_chunk_phase_stamps(tmp_path):
+    """With a buffer past the tile records, the dense epilogue stamps its chunk phases (tcx.h):
+    for each epilogue warp, tiles it ran and chunks 0..CH-1, the seven phase stamps are in
+    order, chunks follow one another, and the tile's accumulator-full wait brackets chunk 0."""
+    code = PROBLEM + """
+M, N, K = 2048, 1024, 256
+A = tcxgen.normal_matrix((M, K), "bf16", 9, tcxgen.STREAM_A, dev)
+B = tcxgen.normal_matrix((N, K), "bf16", 9, tcxgen.STREAM_B, dev)
+C = tcxgen.normal_matrix((M, N), "f32", 9, tcxgen.STREAM_C, dev)
+T, CH = (M // 256) * (N // 256), 8
+buf = torch.zeros(4 * (T + 48 * CH), dtype=torch.int64, device=dev)
+tcx.debug_trace(buf)
+D = tcx.gemm(A, B, C, max_ctas=2)              # one pair: cluster 0 runs all T tiles
+torch.cuda.synchronize()
+tcx.debug_trace(None)
+assert torch.equal(D, tcx.gemm(A, B, C))
+np.save("st.npy", buf[4 * T:].view(4, 6, CH, 8).cpu().numpy())
+print("OK")
+"""
+    r = _run(code, tmp_path)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-2000:]
+    st = np.load(tmp_path / "st.npy").astype(np.int64)          # [warp, tile, chunk, phase]
+    for e in range(4):
+        for t in range(6):
+            s = st[e, t]
+            assert np.all(s[:, :7] > 0), (e, t)
+            assert np.all(np.diff(s[:, :7], axis=1) >= 0), (e, t)              # phases in order
+            assert np.all(s[1:, 0] >= s[:-1, 6]), (e, t)                       # chunks in order
+            assert s[0, 7] <= s[1, 7] <= s[0, 0], (e, t)                       # full-wait, then chunk 0
+            if t:
+                assert st[e, t, 0, 7] >= st[e, t - 1, -1, 6], (e, t)           # tiles in order
