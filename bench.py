@@ -644,11 +644,11 @@ def main():
         return
 
     dist_on = world > 1
+    torch.cuda.set_device(local)                 # before the NCCL group: its barriers use this GPU
+    dev = torch.device("cuda", local)
     if dist_on:
         import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        dist.init_process_group("nccl", init_method="env://", device_id=dev)
     import paper_2206_02874_b200 as tcx
     tcx.lib()
     pk = peaks()
