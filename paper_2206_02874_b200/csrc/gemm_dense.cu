@@ -50,10 +50,14 @@ struct Cfg {
   static constexpr int A_BYTES = BM * KBYTES;                    // 16 KiB
   static constexpr int B_BYTES = NH * HALF_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = NH == 2 ? 4 : (CG == 1 ? 4 : 6);
+  static constexpr int STAGES = NH == 2 ? 3 : (CG == 1 ? 4 : 6);
+  // epilogue staging buffers per warp (4 KiB each) and how far ahead C is loaded: the wide tile's
+  // single accumulator puts the epilogue on the critical path, so it trades a ring stage for depth
+  static constexpr int NBE = NH == 2 ? 4 : 2;
+  static constexpr int C_AHEAD = NBE == 2 ? 2 : NBE - 1;
   static constexpr int NBUF = 2 / NH;                            // TMEM accumulator buffers
   static constexpr int SMEM_DATA = STAGES * STAGE_BYTES;
-  static constexpr int STG_BYTES = EPI_WARPS * 2 * 4096;         // epilogue: 2 x 4 KiB per warp
+  static constexpr int STG_BYTES = EPI_WARPS * NBE * 4096;       // epilogue: NBE x 4 KiB per warp
   static constexpr int SMEM_TOTAL = SMEM_DATA + STG_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
   static_assert(NH == 1 || CG == 2, "wide tiles need the CTA pair");
 };
@@ -81,7 +85,7 @@ struct Smem {
   uint64_t empty[8];
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];      // NH = 1: per buffer; NH = 2: per N-half of the single buffer
-  uint64_t cbar[EPI_WARPS][2]; // epilogue: C chunk landed in staging buffer b of warp e
+  uint64_t cbar[EPI_WARPS][4]; // epilogue: C chunk landed in staging buffer b of warp e
   uint64_t cring[EPI_WARPS];   // epilogue, last tile: all of warp e's C chunks landed in the idle ring
   uint32_t tmem_base;
 };
@@ -152,7 +156,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     for (int s = 0; s < C_::STAGES; ++s) { mbar_init(&sm->full[s], 1); mbar_init(&sm->empty[s], mc ? P : 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&sm->tmem_full[a], 1); mbar_init(&sm->tmem_empty[a], EPI_WARPS * CG); }
     for (int w = 0; w < EPI_WARPS; ++w) {
-      mbar_init(&sm->cbar[w][0], 1); mbar_init(&sm->cbar[w][1], 1); mbar_init(&sm->cring[w], 1);
+      for (int b = 0; b < 4; ++b) mbar_init(&sm->cbar[w][b], 1); mbar_init(&sm->cring[w], 1);
     }
     fence_mbar_init();
   }
@@ -318,7 +322,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     const int e = warp - 4;
     const int lane = threadIdx.x & 31;
     constexpr int CH = BN / 32;
-    uint8_t* stg = smem + C_::SMEM_DATA + e * 8192;
+    uint8_t* stg = smem + C_::SMEM_DATA + e * C_::NBE * 4096;
     uint64_t* cbar = &sm->cbar[e][0];
     uint32_t cph = 0u;                            // bit b: phase of cbar[b] (a register, not a local array)
     const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), lead_rank) : smem_u32(&sm->tmem_empty[0]);
@@ -423,7 +427,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     const int e = warp - 4;                       // TMEM lanes 32e .. 32e+31
     const int lane = threadIdx.x & 31;
     constexpr int CH = NH * BN / 32;              // 32-column chunks per tile (over both halves)
-    uint8_t* stg = smem + C_::SMEM_DATA + e * 8192;
+    uint8_t* stg = smem + C_::SMEM_DATA + e * C_::NBE * 4096;
     uint64_t* cbar = &sm->cbar[e][0];
     uint32_t cph = 0u;                            // bit b: phase of cbar[b] (a register, not a local array)
     const uint32_t tmem_empty_cluster = CG == 2 ? mapa(smem_u32(&sm->tmem_empty[0]), lead_rank) : smem_u32(&sm->tmem_empty[0]);
@@ -455,8 +459,9 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     auto load_c = [&](int64_t q) {
       if (has_c && lane == 0 && q < nq && !(RING_LAST && q >= q_last0)) {
         int x, y; coords(q, x, y);
-        mbar_arrive_expect_tx(&cbar[q & 1], 4096);
-        tma_load_2d(stg + (q & 1) * 4096, &tmC, &cbar[q & 1], x, y);
+        const int bq = (int)(q % C_::NBE);
+        mbar_arrive_expect_tx(&cbar[bq], 4096);
+        tma_load_2d(stg + bq * 4096, &tmC, &cbar[bq], x, y);
       }
     };
     // single-buffered (wide) tiles: the epilogue is on the critical path, so each tile's C is
@@ -467,8 +472,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         for (int ch = 0; ch < CH; ++ch) { int x, y; coords(it * CH + ch, x, y); tma_prefetch_2d(&tmC, x, y); }
     };
     prefetch_c_tile(0);
-    load_c(0);
-    load_c(1);
+    for (int c = 0; c < C_::C_AHEAD; ++c) load_c(c);
     int acc = 0; uint32_t acc_phase = 0;
     const uint32_t lane_off = (uint32_t)(e * 32) << 16;
 #if TCX_WATCHDOG
@@ -506,7 +510,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
 #pragma unroll 1
       for (int ch = 0; ch < CH; ++ch) {
         const int64_t q = it * CH + ch;
-        const int b = (int)(q & 1);
+        const int b = (int)(q % C_::NBE);
         const int h = ch / (BN / 32);
         TCX_STAMP(it, ch, 0);
         tmem_ld_wait();                           // chunk ch has landed in vn
@@ -522,8 +526,8 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         } else if (has_c) {
           mbar_wait(&cbar[b], (cph >> b) & 1u);
           cph ^= 1u << b;
-        } else if (q >= 2) {
-          if (lane == 0) bulk_wait_read<1>();     // the store of chunk q-2 has read buffer b
+        } else if (q >= C_::NBE) {
+          if (lane == 0) bulk_wait_read<C_::NBE - 1>();   // the store of chunk q-NBE has read buffer b
           __syncwarp();
         }
         TCX_STAMP(it, ch, 2);
@@ -567,11 +571,12 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           tma_store_2d(&tmD, buf, x, y);
           bulk_commit();
           TCX_STAMP(it, ch, 5);
-          if (!ring && has_c && q + 2 < nq && !(RING_LAST && q + 2 >= q_last0))
-            bulk_wait_read<0>();                              // buffer b is free again ...
+          // the buffer of chunk q + C_AHEAD was last read by the store of chunk q + C_AHEAD - NBE
+          if (!ring && has_c && q + C_::C_AHEAD < nq && !(RING_LAST && q + C_::C_AHEAD >= q_last0))
+            bulk_wait_read<C_::NBE - C_::C_AHEAD>();
         }
         TCX_STAMP(it, ch, 6);
-        if (!ring) load_c(q + 2);                             // ... for the C chunk two ahead
+        if (!ring) load_c(q + C_::C_AHEAD);
       }
 #if TCX_WATCHDOG
       if (trace && e == 0 && lane == 0 && rank == 0) {
