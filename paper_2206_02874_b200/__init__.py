@@ -50,14 +50,16 @@ class GemmOpts(ctypes.Structure):
 
 class ProbeConfig(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in ("kind", "ab", "cd", "m", "n", "k", "cta_group", "warps", "ilp",
-                                             "iters", "repeats", "num_sms")]
+                                             "iters", "repeats", "num_sms", "issuers", "n_acc", "mode")] + \
+               [("a_op", ctypes.c_void_p), ("b_op", ctypes.c_void_p), ("acc_out", ctypes.c_void_p)]
 
 
 class ProbeResult(ctypes.Structure):
     _fields_ = [("cycles_per_iter_min", ctypes.c_double), ("cycles_per_iter_median", ctypes.c_double),
                 ("latency_cycles", ctypes.c_double), ("fma_per_clk_per_sm", ctypes.c_double),
                 ("sm_mhz", ctypes.c_double), ("ns_per_iter", ctypes.c_double), ("iters", ctypes.c_int64),
-                ("sink", ctypes.c_uint32)]
+                ("sink", ctypes.c_uint32), ("mmas_per_issuer", ctypes.c_int64), ("warmup_iters", ctypes.c_int32),
+                ("n_acc", ctypes.c_int32), ("sms_used", ctypes.c_int32), ("max_issuers_per_sm", ctypes.c_int32)]
 
 
 _lib = None
@@ -136,25 +138,54 @@ def ab_code(t: torch.Tensor, tf32: bool = False) -> int:
 
 
 def _dev_check(*ts):
+    ts = [t for t in ts if t is not None]
     for t in ts:
-        if t is not None and not t.is_cuda:
+        if not t.is_cuda:
             raise ValueError("tcx operates on CUDA tensors only (no CPU fallback)")
+    if len({t.device for t in ts}) > 1:
+        raise ValueError("tcx: all tensors of a call must be on one CUDA device")
+
+
+_CD_TORCH = {F32: torch.float32, S32: torch.int32, F16: torch.float16}
+
+
+def _need(cond, msg):
+    if not cond:
+        raise ValueError(msg)
+
+
+def _rows_ok(name, t, shape, dtype):
+    """t is a 2-D (or N-D) tensor of `shape` and `dtype` whose innermost stride is 1 (rows may be
+    padded: the C ABI takes the row stride); raised before any pointer reaches the library, so a
+    mismatched buffer can never be read or written out of bounds by the TMA engine"""
+    _need(t.dim() == len(shape), f"{name}: expected {len(shape)}-D, got shape {tuple(t.shape)}")
+    _need(tuple(t.shape) == tuple(shape), f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    _need(t.dtype == dtype, f"{name}: expected dtype {dtype}, got {t.dtype}")
+    _need(t.numel() == 0 or t.stride(-1) == 1, f"{name}: the innermost dimension must be contiguous (stride 1)")
+    if t.dim() > 2:
+        _need(t.is_contiguous(), f"{name}: must be contiguous")
 
 
 # ---------------------------------------------------------------------------------------- tiles
 def mma_tiles(A, B, C=None, D=None, tf32=False, tc05=False, f16_acc=False):
     """D_t = A_t B_t + C_t for A (count, 16, k), B (count, 8, k), C/D (count, 16, 8).
     f16_acc: C/D are FP16 (the f16.f16.f16.f16 MMA); C, if given, must be float16."""
-    _dev_check(A, B, C, D)
     ab = ab_code(A, tf32)
+    _need(A.dim() == 3, f"A: expected (count, 16, k), got shape {tuple(A.shape)}")
     count, m, k = A.shape
-    n = B.shape[1]
+    n = 8
     cd = S32 if ab == S8 else (F16 if f16_acc else F32)
     if C is not None and cd == F16 and C.dtype != torch.float16:
         raise ValueError("f16_acc: C must be float16")
+    _rows_ok("A", A, (count, m, k), A.dtype)
+    _rows_ok("B", B, (count, n, k), A.dtype)
+    if C is not None:
+        _rows_ok("C", C, (count, m, n), _CD_TORCH[cd])
+    if D is not None:
+        _rows_ok("D", D, (count, m, n), _CD_TORCH[cd])
+    _dev_check(A, B, C, D)
     if D is None:
-        D = torch.empty((count, m, n), dtype={S32: torch.int32, F16: torch.float16, F32: torch.float32}[cd],
-                        device=A.device)
+        D = torch.empty((count, m, n), dtype=_CD_TORCH[cd], device=A.device)
     fn = lib().tcx_mma_tiles_tc05 if tc05 else lib().tcx_mma_tiles
     _check(fn(ab, cd, m, n, k, count, _ptr(A), _ptr(B), _ptr(C), _ptr(D), _stream(A)))
     return D
@@ -184,15 +215,22 @@ def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, t
     """Dense D = A x B + C with A (M, K), B stored (N, K) ("row.col"), C/D (M, N).
     f16_acc: FP16 inputs with an FP16 accumulator (C, D float16; C is the MMA's C operand).
     pairs = (pairs_m, pairs_n): TMA-multicast cluster of CTA pairs (tcx_gemm_opts)."""
-    _dev_check(A, B, C, D)
     ab = ab_code(A, tf32)
+    _need(A.dim() == 2 and B.dim() == 2, "gemm: A (M, K) and B (N, K) must be 2-D")
     M, K = A.shape
     N = B.shape[0]
     cd = S32 if ab == S8 else (F16 if f16_acc else F32)
     if cd == F16 and C is not None and C.dtype != torch.float16:
         raise ValueError("f16_acc: C must be float16")
+    _rows_ok("A", A, (M, K), A.dtype)
+    _rows_ok("B", B, (N, K), A.dtype)
+    if C is not None:
+        _rows_ok("C", C, (M, N), _CD_TORCH[cd])
+    if D is not None:
+        _rows_ok("D", D, (M, N), _CD_TORCH[cd])
+    _dev_check(A, B, C, D)
     if D is None:
-        D = torch.empty((M, N), dtype={S32: torch.int32, F16: torch.float16, F32: torch.float32}[cd], device=A.device)
+        D = torch.empty((M, N), dtype=_CD_TORCH[cd], device=A.device)
     ldc = C.stride(0) if C is not None else N
     if not (cta_group or max_ctas or group_m or tile_n or pairs[0] or pairs[1] or _fault):
         _check(lib().tcx_gemm(ab, cd, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(C), ldc, _ptr(D),
@@ -219,9 +257,11 @@ def sp24_compress(A_dense, tf32=False):
     """dense (M, K) 2:4 matrix -> (vals (M, K/2), meta_canon (M, K/32) int32).
     Raises ValueError naming the first (row, group) with more than 2 nonzeros.  tf32=True (FP32
     storage): the hardware's 1:2 rule — one element kept per aligned pair."""
-    _dev_check(A_dense)
     ab = ab_code(A_dense, tf32)
+    _need(A_dense.dim() == 2, "sp24_compress: A must be 2-D")
     M, K = A_dense.shape
+    _rows_ok("A", A_dense, (M, K), A_dense.dtype)
+    _dev_check(A_dense)
     vals = torch.empty((M, K // 2), dtype=A_dense.dtype, device=A_dense.device)
     meta = torch.empty((M, K // 32), dtype=torch.int32, device=A_dense.device)
     bad = torch.empty(2, dtype=torch.int64, device=A_dense.device)
@@ -238,6 +278,8 @@ def sp24_meta_hw_bytes(M, K, ab=F16):
 
 
 def sp24_pack_meta(meta_canon, M, K, ab=F16, check=True):
+    _rows_ok("meta_canon", meta_canon, (M, K // 32), torch.int32)
+    _need(meta_canon.is_contiguous(), "meta_canon must be contiguous")
     _dev_check(meta_canon)
     nbytes = sp24_meta_hw_bytes(M, K, ab)
     hw = torch.empty(nbytes, dtype=torch.uint8, device=meta_canon.device)
@@ -253,13 +295,25 @@ def sp24_pack_meta(meta_canon, M, K, ab=F16, check=True):
 def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m=0, tf32=False, tile_m=0, pairs=(0, 0)):
     """D = expand(vals, meta) x B + C; vals (M, K/2), B (N, K).  FP16/BF16 -> FP32, INT8 -> INT32
     (meta_hw packed with the same ab: sp24_pack_meta(meta, M, K, ab=S8) for int8)."""
-    _dev_check(vals, meta_hw, B, C, D)
     ab = ab_code(vals, tf32)
+    _need(vals.dim() == 2 and B.dim() == 2, "gemm_sp24: vals (M, K/2) and B (N, K) must be 2-D")
     M = vals.shape[0]
     N, K = B.shape
     cd = S32 if ab == S8 else F32
+    _rows_ok("vals", vals, (M, K // 2), vals.dtype)
+    _need(2 * vals.shape[1] == K, f"gemm_sp24: vals has {vals.shape[1]} kept columns, B's K = {K} needs {K // 2}")
+    _rows_ok("B", B, (N, K), vals.dtype)
+    _need(meta_hw.dtype == torch.uint8 and meta_hw.is_contiguous(), "gemm_sp24: meta_hw must be a contiguous uint8 "
+          "tensor from sp24_pack_meta")
+    _need(meta_hw.numel() == sp24_meta_hw_bytes(M, K, ab),
+          f"gemm_sp24: meta_hw has {meta_hw.numel()} bytes, ({M}, {K}) needs {sp24_meta_hw_bytes(M, K, ab)}")
+    if C is not None:
+        _rows_ok("C", C, (M, N), _CD_TORCH[cd])
+    if D is not None:
+        _rows_ok("D", D, (M, N), _CD_TORCH[cd])
+    _dev_check(vals, meta_hw, B, C, D)
     if D is None:
-        D = torch.empty((M, N), dtype=torch.int32 if cd == S32 else torch.float32, device=vals.device)
+        D = torch.empty((M, N), dtype=_CD_TORCH[cd], device=vals.device)
     opts = GemmOpts(cta_group, max_ctas, group_m, int(tile_m), pairs[0], pairs[1])
     _check(lib().tcx_gemm_sp24_ex(ab, cd, M, N, K, _ptr(vals), vals.stride(0), _ptr(meta_hw), _ptr(B), B.stride(0),
                                   _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
@@ -268,6 +322,10 @@ def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m
 
 
 def round_tf32(x, out=None):
+    _need(x.dtype == torch.float32 and x.is_contiguous(), "round_tf32: x must be a contiguous float32 tensor")
+    if out is not None:
+        _need(out.dtype == torch.float32 and out.is_contiguous() and out.numel() == x.numel(),
+              "round_tf32: out must be a contiguous float32 tensor of x's size")
     _dev_check(x, out)
     if out is None:
         out = torch.empty_like(x)
@@ -278,12 +336,20 @@ def round_tf32(x, out=None):
 # ---------------------------------------------------------------------------------------- probe
 PROBE_KINDS = {"mma_sync": 0, "mma_sp_sync": 1, "tc05": 2, "tc05_sp": 3, "ldmatrix": 4, "ld_shared": 5,
                "tmem_ld": 6, "tma_load": 7, "tc05_cp": 8, "tma_multicast": 9}
+TC05_MODES = {"sync": 0, "stream": 1, "commit": 2}
 
 
 def probe(kind="mma_sync", ab=F16, cd=F32, m=16, n=8, k=16, cta_group=1, warps=1, ilp=1, iters=1024,
-          repeats=5, num_sms=1, device=-1):
+          repeats=5, num_sms=1, device=-1, issuers=0, n_acc=0, mode="sync", a_op=None, b_op=None, acc_out=None):
+    """tcx_probe (include/tcx.h).  tcgen05 kinds: issuers per SM, n_acc accumulators, mode in
+    {"sync", "stream", "commit"}; a_op / b_op / acc_out: optional CUDA tensors (operands and issuer 0's
+    accumulators, layouts in tcx.h)."""
+    for t in (a_op, b_op, acc_out):
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError("probe: a_op / b_op / acc_out must be contiguous CUDA tensors")
     cfg = ProbeConfig(PROBE_KINDS[kind] if isinstance(kind, str) else kind, ab, cd, m, n, k, cta_group, warps, ilp,
-                      iters, repeats, num_sms)
+                      iters, repeats, num_sms, issuers, n_acc, TC05_MODES[mode] if isinstance(mode, str) else mode,
+                      _ptr(a_op), _ptr(b_op), _ptr(acc_out))
     res = ProbeResult()
     _check(lib().tcx_probe(device, ctypes.byref(cfg), ctypes.byref(res)))
     return {f: getattr(res, f) for f, _ in ProbeResult._fields_}

@@ -250,6 +250,9 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
       return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: pairs_m and pairs_n must be 0, 1 or 2");
     if ((pm > 1 || pn > 1) && (g.cta_group != 2 || g.tile_n == 512))
       return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: multicast clusters need cta_group 2 and the 256-wide tile");
+    if (g.tile_n == 512 && (g.cta_group != 2 || cd == TCX_F16))
+      return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm: tile_n 512 (the 256 x 512 pair tile) needs cta_group 2 and a "
+                       "32-bit accumulator");
     g.pairs_m = pm;
     g.pairs_n = pn;
 #if TCX_WATCHDOG
@@ -331,7 +334,9 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
   if (!meta_hw || !aligned16(meta_hw)) return set_error(TCX_ERR_MISALIGNED, "tcx_gemm_sp24: meta_hw NULL or misaligned");
   GemmArgs g{ab, cd, M, N, K, A_vals, lda_vals, B, ldb, C, ldc, D, ldd, meta_hw, 2, 0, 0, 0};
   if (opts) {
-    if (opts->cta_group == 1 || opts->cta_group == 2) g.cta_group = opts->cta_group;
+    if (opts->cta_group != 0 && opts->cta_group != 1 && opts->cta_group != 2)
+      return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm_sp24: cta_group must be 0, 1 or 2");
+    if (opts->cta_group) g.cta_group = opts->cta_group;
     g.max_ctas = opts->max_ctas;
     g.group_m = opts->group_m;
     if (opts->tile_n != 0 && opts->tile_n != 256 && opts->tile_n != 512)
@@ -342,6 +347,9 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
       return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm_sp24: pairs_m and pairs_n must be 0, 1 or 2");
     if ((pm > 1 || pn > 1) && (g.cta_group != 2 || g.tile_n == 512))
       return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm_sp24: multicast groups need cta_group 2 and the 256-row tile");
+    if (g.tile_n == 512 && (g.cta_group != 2 || ab == TCX_S8 || M % 512))
+      return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: tile_n 512 (the 512 x 240 pair tile) needs cta_group 2, "
+                       "F16/BF16/TF32 and M %% 512 == 0");
     g.pairs_m = pm;
     g.pairs_n = pn;
   }

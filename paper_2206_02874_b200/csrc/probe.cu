@@ -153,30 +153,102 @@ tcx_status launch_probe_mma(int ilp, int grid, int warps, int iters, long long* 
 }
 
 // ------------------------------------------------------------------ tcgen05 probe
-// One CTA (or CTA pair) per SM; thread 0 of the leader issues ILP MMAs per iteration into up to
-// n_acc distinct accumulators, commits to an mbarrier and waits for it.
+// The paper's method re-cast for the asynchronous, single-thread-issued tcgen05.mma
+// (SURVEY §8(a6)): one elected thread per issuing CTA (pair) is the "warp"; up to two issuing CTAs
+// share an SM (`issuers`, each with 512 / issuers TMEM columns) — the analogue of #warps per SM;
+// ILP = MMAs issued per iteration, rotating over n_acc independent accumulators (n_acc = 1: one
+// dependent chain into one accumulator, the GEMM mainloop pattern).  Modes:
+//   SYNC    every iteration ends with tcgen05.commit -> mbarrier wait (the paper's per-iteration
+//           sync); ILP 1 gives the completion latency (MMA + commit round trip)
+//   STREAM  ITERS x ILP MMAs back to back, one commit + wait at the end: the pipe's issue-limited rate
+//   COMMIT  ITERS x (commit -> wait) with no MMA: the commit round trip alone (latency split)
+// Operands (optional) are copied from global into the 128B-swizzled smem tiles the MMAs read; the
+// accumulators of one issuer (the first active one to finish) can be read back (acc_out) so a test can check the MMA count exactly.
+// Issuers whose SM (rank 0's %smid) is >= num_sms exit before touching TMEM (issuers = 2 launches
+// two CTAs per SM on every SM — the smem request caps residency at two — and keeps num_sms of them).
+struct Tc05ProbeArgs {
+  int mode, iters, ilp, n_acc, acc_cols, alloc_cols, num_sms, a_bytes, b_bytes, n_rows;
+  uint32_t idesc;
+  const uint8_t* a_op;
+  const uint8_t* b_op;
+  long long* cycles;
+  long long* ns;
+  int* smid_out;
+  uint32_t* acc_out;
+  int* claim;        // the first active issuer to finish writes acc_out (zeroed per launch)
+  int* arrive;       // issuers = 2: CTAs resident so far (zeroed per launch)
+  long long* g0;     // per issuer: %globaltimer at the start / end of the timed region
+  long long* g1;
+};
+constexpr int TC05_WARMUP = 2;
+constexpr int TC05_META_COLS = 8;
+
 template <int CG, int KIND, bool SPARSE>
 __global__ void __launch_bounds__(128, 1)
-probe_tc05_kernel(int iters, int ilp, int n_acc, int acc_cols, uint32_t idesc, long long* cycles, long long* ns) {
+probe_tc05_kernel(const Tc05ProbeArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sa = smem;                 // 128 rows x 128 B
-  uint8_t* sb = smem + 16384;         // 256 rows x 128 B
+  uint8_t* sa = smem;                 // 128 rows x 128 B (SW128)
+  uint8_t* sb = smem + 16384;         // up to 256 rows x 128 B (SW128)
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base_s;
+  __shared__ int smid_s;
   const int warp = threadIdx.x / 32;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  if (threadIdx.x == 0) {
+    int sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    smid_s = sm;
+  }
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  int lead_smid = smid_s;
+  if constexpr (CG == 2) {
+    uint32_t a = mapa(smem_u32(&smid_s), 0);
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(lead_smid) : "r"(a) : "memory");
+  }
+  const bool active = lead_smid < p.num_sms;
+  if (threadIdx.x == 0) {
+    p.smid_out[blockIdx.x] = active ? smid_s : -1;
+    if (p.num_sms < (1 << 30)) {
+      // issuers = 2: a gated CTA keeps its slot until every CTA of the grid is resident (the grid is
+      // two per SM, which the smem request makes the occupancy, so all are co-resident), so no
+      // later CTA is placed on an SM a gated one vacated
+      atomicAdd(p.arrive, 1);
+      while (*(volatile int*)p.arrive < (int)gridDim.x) __nanosleep(256);
+    }
+  }
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();   // peer's smid read before anyone exits
+  if (!active) return;
+  // operands: this CTA's A rows (rank * 128 ..) and B rows (rank * n_rows ..), SW128 placement
   for (int i = threadIdx.x; i < (16384 + 32768) / 16; i += blockDim.x) ((uint4*)smem)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  if (p.a_op) {
+    const int ch = p.a_bytes / 16;
+    for (int i = threadIdx.x; i < 128 * ch; i += blockDim.x) {
+      const int r = i / ch, c = i % ch;
+      *(uint4*)(sa + r * 128 + ((c ^ (r % 8)) * 16)) = *(const uint4*)(p.a_op + ((int64_t)rank * 128 + r) * p.a_bytes + c * 16);
+    }
+  }
+  if (p.b_op) {
+    const int ch = p.b_bytes / 16;
+    for (int i = threadIdx.x; i < p.n_rows * ch; i += blockDim.x) {
+      const int r = i / ch, c = i % ch;
+      *(uint4*)(sb + r * 128 + ((c ^ (r % 8)) * 16)) = *(const uint4*)(p.b_op + ((int64_t)rank * p.n_rows + r) * p.b_bytes + c * 16);
+    }
+  }
   fence_proxy_async_smem();
   if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
-  if (warp == 0) { tmem_alloc<CG>(&tmem_base_s, 512); tmem_relinquish<CG>(); }
+  if (warp == 0) {
+    if (p.alloc_cols == 512) tmem_alloc<CG>(&tmem_base_s, 512); else tmem_alloc<CG>(&tmem_base_s, 256);
+    tmem_relinquish<CG>();
+  }
   tc05_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc05_fence_after();
   const uint32_t tbase = tmem_base_s;
-  const uint32_t tmeta = tbase + 448;
+  const uint32_t tmeta = tbase + p.alloc_cols - TC05_META_COLS;
   if constexpr (SPARSE) {
-    // metadata = all (0,1) pairs (nibble 0x4) in columns 448..455 of every lane
+    // metadata: every 4-group keeps positions (0, 1) (nibble 0x4) in the metadata columns of every
+    // lane (TF32: the first element of every aligned pair)
     uint32_t r8[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) r8[j] = 0x44444444u;
@@ -186,52 +258,112 @@ probe_tc05_kernel(int iters, int ilp, int n_acc, int acc_cols, uint32_t idesc, l
   tc05_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc05_fence_after();
-  if (rank == 0 && threadIdx.x == 0) {
+  // the issuer: warp 0 of the leader CTA runs the loop converged (warp-uniform addresses live in
+  // uniform registers) and one elected lane issues each iteration's MMAs, as the GEMMs' MMA warp does
+  if (rank == 0 && warp == 0) {
     const uint64_t ad = sdesc(smem_u32(sa), 16, 1024, 2);
     const uint64_t bd = sdesc(smem_u32(sb), 16, 1024, 2);
+    const int ilp = p.ilp, n_acc = p.n_acc;
+    const uint32_t acc_step = (uint32_t)p.acc_cols;
     uint32_t phase = 0;
-    long long t0 = 0; uint64_t g0 = 0;
-    for (int it = -2; it < iters; ++it) {
-      if (it == 0) { t0 = clock64(); g0 = globaltimer(); }
-      for (int i = 0; i < ilp; ++i) {
-        const uint32_t d = tbase + (uint32_t)((i % n_acc) * acc_cols);
-        if constexpr (SPARSE) umma_sp<CG, KIND>(d, ad, bd, tmeta, idesc, 1u);
-        else umma<CG, KIND>(d, ad, bd, idesc, 1u);
+    auto mma_iter = [&](uint32_t first) {
+      if (elect_one()) {
+        uint32_t d = tbase;
+        int a = 0;
+        for (int i = 0; i < ilp; ++i) {
+          const uint32_t acc = (first && i < n_acc) ? 0u : 1u;   // first use of an accumulator: D = A.B
+          if constexpr (SPARSE) umma_sp<CG, KIND>(d, ad, bd, tmeta, p.idesc, acc);
+          else umma<CG, KIND>(d, ad, bd, p.idesc, acc);
+          d += acc_step;
+          if (++a == n_acc) { a = 0; d = tbase; }
+        }
       }
-      if constexpr (CG == 1)
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_u32(&bar)) : "memory");
-      else
-        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-                     :: "r"(smem_u32(&bar)), "h"((uint16_t)1) : "memory");
+      __syncwarp();
+    };
+    auto commit_wait = [&]() {
+      if (elect_one()) {
+        if constexpr (CG == 1)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_u32(&bar)) : "memory");
+        else
+          asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                       :: "r"(smem_u32(&bar)), "h"((uint16_t)1) : "memory");
+      }
+      __syncwarp();
       mbar_wait(&bar, phase);
       phase ^= 1;
       tc05_fence_after();
+    };
+    const bool mmas = p.mode != 2;
+    for (int it = 0; it < TC05_WARMUP; ++it) {
+      if (mmas) mma_iter(it == 0);
+      commit_wait();
+    }
+    const long long t0 = clock64();
+    const uint64_t g0 = globaltimer();
+    if (p.mode == 1) {
+      for (int it = 0; it < p.iters; ++it) mma_iter(0);
+      commit_wait();
+    } else {
+      for (int it = 0; it < p.iters; ++it) {
+        if (mmas) mma_iter(0);
+        commit_wait();
+      }
     }
     const long long t1 = clock64();
     const uint64_t g1 = globaltimer();
-    cycles[blockIdx.x / CG] = t1 - t0;
-    ns[blockIdx.x / CG] = (long long)(g1 - g0);
+    if (threadIdx.x == 0) {
+      p.cycles[blockIdx.x / CG] = t1 - t0;
+      p.ns[blockIdx.x / CG] = (long long)(g1 - g0);
+      p.g0[blockIdx.x / CG] = (long long)g0;
+      p.g1[blockIdx.x / CG] = (long long)g1;
+    }
+  }
+  __shared__ int writer_s;
+  if (threadIdx.x == 0 && rank == 0) {
+    const int w = p.acc_out ? (atomicCAS(p.claim, 0, 1) == 0) : 0;
+    writer_s = w;
+    if constexpr (CG == 2) asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(mapa(smem_u32(&writer_s), 1)), "r"(w) : "memory");
   }
   tc05_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
-  if (warp == 0) { tc05_fence_after(); tmem_dealloc<CG>(tbase, 512); }
+  tc05_fence_after();
+  if (writer_s) {
+    // issuer 0's accumulators: acc_out[a][rank * 128 + lane row][col], 32-bit words
+    const int lane = threadIdx.x & 31;
+    const int row = (int)rank * 128 + warp * 32 + lane;
+    const int rows = 128 * CG;
+    for (int a = 0; a < p.n_acc; ++a)
+      for (int c0 = 0; c0 < p.acc_cols; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(tbase + a * p.acc_cols + c0 + ((uint32_t)(warp * 32) << 16), v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) p.acc_out[((int64_t)a * rows + row) * p.acc_cols + c0 + j] = v[j];
+      }
+  }
+  tc05_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if (warp == 0) {
+    tc05_fence_after();
+    if (p.alloc_cols == 512) tmem_dealloc<CG>(tbase, 512); else tmem_dealloc<CG>(tbase, 256);
+  }
 }
 
 template <int CG, int KIND, bool SPARSE>
-tcx_status launch_probe_tc05(int clusters, int iters, int ilp, int n_acc, int acc_cols, uint32_t idesc,
-                             long long* cyc, long long* ns) {
+tcx_status launch_probe_tc05(int grid_ctas, int issuers, const Tc05ProbeArgs& a) {
   auto kern = probe_tc05_kernel<CG, KIND, SPARSE>;
-  const int smem = 16384 + 32768 + 1024;
+  // 49 KiB of operands; two issuers per SM: request enough smem that at most two CTAs fit an SM
+  const int smem = issuers == 2 ? 100 * 1024 : 16384 + 32768 + 1024;
   TCX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(clusters * CG);
+  cfg.gridDim = dim3(grid_ctas);
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr; cfg.numAttrs = 1;
-  TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, iters, ilp, n_acc, acc_cols, idesc, cyc, ns));
+  TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a));
   count_launch();
   return TCX_OK;
 }
@@ -353,6 +485,7 @@ tcx_status launch_tiles_tc05(tcx_dtype ab, int k, int64_t count, const void* A, 
 }
 
 tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_result* out) {
+  *out = tcx_probe_result{};
   const int iters = cfg->iters > 0 ? cfg->iters : 1024;
   const int reps = cfg->repeats > 0 ? cfg->repeats : 5;
   const int nsm = cfg->num_sms > 0 ? std::min(cfg->num_sms, dev.sm_count) : 1;
@@ -426,9 +559,11 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
   } else if (cfg->kind == TCX_PROBE_TC05 || cfg->kind == TCX_PROBE_TC05_SP) {
     const bool sp = cfg->kind == TCX_PROBE_TC05_SP;
     const int cg = cfg->cta_group == 2 ? 2 : 1;
+    const int issuers = cfg->issuers > 0 ? cfg->issuers : 1;
+    const int mode = cfg->mode;
     int kind;
     uint32_t fmt;
-    int kbytes = sp ? 64 : 32;
+    const int kbytes = sp ? 64 : 32;           // logical K bytes of one MMA (B operand row bytes)
     if (ab == TCX_F16 || ab == TCX_BF16) { kind = KIND_F16; fmt = ab == TCX_BF16 ? 1 : 0; }
     else if (ab == TCX_TF32) { kind = KIND_TF32; fmt = 2; }
     else if (ab == TCX_S8) { kind = KIND_I8; fmt = 1; }
@@ -436,21 +571,44 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
     const int esz = ab == TCX_S8 ? 1 : (ab == TCX_TF32 ? 4 : 2);
     const int kexp = kbytes / esz;
     if (k != kexp) { st = set_error(TCX_ERR_UNSUPPORTED, "tcx_probe: tcgen05 K must be %d for this kind", kexp); goto done; }
+    if (issuers != 1 && issuers != 2) { st = set_error(TCX_ERR_INVALID_VALUE, "tcx_probe: issuers must be 1 or 2"); goto done; }
+    if (mode < 0 || mode > 2) { st = set_error(TCX_ERR_INVALID_VALUE, "tcx_probe: tcgen05 mode must be 0, 1 or 2"); goto done; }
     const bool mok = cg == 1 ? (m == 64 || m == 128) : (m == 128 || m == 256);
     const bool nok = n >= 16 && n <= 256 && n % 16 == 0;
     if (!mok || !nok) { st = set_error(TCX_ERR_UNSUPPORTED, "tcx_probe: tcgen05 M/N"); goto done; }
+    const int alloc_cols = 512 / issuers;
+    const int avail = alloc_cols - (sp ? TC05_META_COLS : 0);
+    const int max_acc = avail / n;
+    if (max_acc < 1) { st = set_error(TCX_ERR_UNSUPPORTED, "tcx_probe: N = %d does not fit %d TMEM columns", n, avail); goto done; }
+    const int n_acc = cfg->n_acc > 0 ? cfg->n_acc : std::min(ilp, max_acc);
+    if (n_acc > max_acc || n_acc > ilp) {
+      st = set_error(TCX_ERR_INVALID_VALUE, "tcx_probe: n_acc %d must be <= ilp (%d) and <= %d", n_acc, ilp, max_acc); goto done;
+    }
+    if ((cfg->acc_out || cfg->a_op || cfg->b_op) && m != 128 * cg) {
+      st = set_error(TCX_ERR_UNSUPPORTED, "tcx_probe: operands / acc_out need M = 128 per CTA"); goto done;
+    }
     const uint32_t cfmt = ab == TCX_S8 ? 2u : 1u;
     const uint32_t idesc = (sp ? (1u << 2) : 0u) | (cfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(n >> 3) << 17) |
                            ((uint32_t)(m >> 4) << 24);
-    const int acc_cols = n;
-    const int max_acc = (sp ? 448 : 512) / acc_cols;
-    // independent accumulators the ILP MMAs rotate over (cfg->warps > 0 caps it; 1 = one chain)
-    const int n_acc = std::max(1, std::min(cfg->warps > 0 ? std::min(ilp, cfg->warps) : ilp, max_acc));
-    const int clusters = std::max(1, nsm / cg);
-    issuers_per_sm = 1.0 / cg;           // one MMA stream per CTA pair covers 2 SMs
-    mnk = (double)m * n * k;
+    // issuers = 1: num_sms CTAs (pairs), one per SM; issuers = 2: two CTAs on every SM, the clusters
+    // whose leader sits on SM >= num_sms exit at once
+    const int grid = issuers == 1 ? std::max(1, nsm / cg) * cg : dev.sm_count * 2;
+    const int nclusters = grid / cg;
+    int* d_smid = nullptr;
+    TCX_CUDA_TRY(cudaMalloc(&d_smid, (grid + 2) * sizeof(int)));
+    long long* d_t = nullptr;              // cycles, ns, g0, g1 per issuer
+    TCX_CUDA_TRY(cudaMalloc(&d_t, 4 * nclusters * sizeof(long long)));
+    Tc05ProbeArgs pa{mode, iters, ilp, n_acc, n, alloc_cols, issuers == 1 ? 1 << 30 : nsm, 32, kbytes, n / cg, idesc,
+                     (const uint8_t*)cfg->a_op, (const uint8_t*)cfg->b_op, d_t, d_t + nclusters,
+                     d_smid, (uint32_t*)cfg->acc_out, d_smid + grid, d_smid + grid + 1, d_t + 2 * nclusters,
+                     d_t + 3 * nclusters};
+    std::vector<int> smid(grid);
+    std::vector<double> rate;               // FMA per clk per SM over the union of the issuers' timed regions
+    int used = 0, mx = 0;
     for (int rep = 0; rep < reps && st == TCX_OK; ++rep) {
-#define T(CGV, KV, SPV) st = launch_probe_tc05<CGV, KV, SPV>(clusters, iters, ilp, n_acc, acc_cols, idesc, d_cyc, d_ns)
+      TCX_CUDA_TRY(cudaMemset(pa.cycles, 0xff, nclusters * sizeof(long long)));
+      TCX_CUDA_TRY(cudaMemset(pa.claim, 0, 2 * sizeof(int)));
+#define T(CGV, KV, SPV) st = launch_probe_tc05<CGV, KV, SPV>(grid, issuers, pa)
       if (cg == 1) {
         if (kind == KIND_F16) { if (sp) T(1, KIND_F16, true); else T(1, KIND_F16, false); }
         else if (kind == KIND_TF32) { if (sp) T(1, KIND_TF32, true); else T(1, KIND_TF32, false); }
@@ -464,16 +622,52 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
       if (st != TCX_OK) break;
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { st = set_error(TCX_ERR_CUDA, "probe kernel: %s", cudaGetErrorString(e)); break; }
-      std::vector<long long> cyc(clusters), nsv(clusters);
-      cudaMemcpy(cyc.data(), d_cyc, cyc.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-      cudaMemcpy(nsv.data(), d_ns, nsv.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-      std::vector<double> c2(cyc.begin(), cyc.end()), n2(nsv.begin(), nsv.end());
+      std::vector<long long> t(4 * nclusters);
+      cudaMemcpy(t.data(), d_t, t.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+      cudaMemcpy(smid.data(), d_smid, grid * sizeof(int), cudaMemcpyDeviceToHost);
+      std::vector<double> c2, n2, ghz;
+      long long gmin = 0, gmax = 0;
+      int active = 0;
+      for (int c = 0; c < nclusters; ++c) {
+        if (t[c] < 0) continue;                                 // gated issuer
+        c2.push_back((double)t[c]); n2.push_back((double)t[nclusters + c]);
+        if (t[nclusters + c] > 0) ghz.push_back((double)t[c] / (double)t[nclusters + c]);
+        const long long a = t[2 * nclusters + c], b = t[3 * nclusters + c];
+        if (active++ == 0) { gmin = a; gmax = b; } else { gmin = std::min(gmin, a); gmax = std::max(gmax, b); }
+      }
+      // latency: the median issuer's cycles per iteration (the paper's per-warp clock counters)
       per_iter.push_back(median(c2) / iters);
       per_ns.push_back(median(n2) / iters);
+      std::vector<int> per_sm(4096, 0);
+      used = 0; mx = 0;
+      for (int c = 0; c < grid; ++c)
+        if (smid[c] >= 0 && smid[c] < 4096) { if (per_sm[smid[c]]++ == 0) ++used; mx = std::max(mx, per_sm[smid[c]]); }
+      // throughput: every active issuer's MMAs over the union of their timed regions (global timer,
+      // converted with the measured SM clock), per SM used
+      const double span_cyc = (double)(gmax - gmin) * median(ghz);
+      if (used > 0 && span_cyc > 0)
+        rate.push_back((double)active * iters * (mode == 2 ? 0 : ilp) * m * n * k / ((double)used * span_cyc));
     }
-    // throughput per SM: ILP MMAs of m x n x k per iteration, spread over cg SMs
-    issuers_per_sm = 1.0 / cg;
-    mnk = (double)m * n * k * ilp;
+    if (st == TCX_OK) {
+      out->sms_used = used;
+      out->max_issuers_per_sm = mx;
+      out->mmas_per_issuer = mode == 2 ? 0 : (int64_t)iters * ilp;
+      out->warmup_iters = TC05_WARMUP;
+      out->n_acc = n_acc;
+    }
+    cudaFree(d_smid);
+    cudaFree(d_t);
+    if (st == TCX_OK && !per_iter.empty()) {
+      const double med = median(per_iter);
+      out->cycles_per_iter_min = *std::min_element(per_iter.begin(), per_iter.end());
+      out->cycles_per_iter_median = med;
+      out->latency_cycles = med;
+      out->ns_per_iter = median(per_ns);
+      out->sm_mhz = out->ns_per_iter > 0 ? med / out->ns_per_iter * 1000.0 : 0;
+      out->fma_per_clk_per_sm = rate.empty() ? 0.0 : median(rate);
+      out->iters = iters;
+    }
+    goto done;
   } else if (cfg->kind == TCX_PROBE_LDMATRIX || cfg->kind == TCX_PROBE_LDSHARED || cfg->kind == TCX_PROBE_TMEM_LD ||
              cfg->kind == TCX_PROBE_TMA_LOAD || cfg->kind == TCX_PROBE_TC05_CP ||
              cfg->kind == TCX_PROBE_TMA_MULTICAST) {

@@ -48,6 +48,8 @@ def _opts(**kw):
     (dict(opts=_opts(pairs_m=3)), INVALID),
     (dict(opts=_opts(pairs_m=2, cta_group=1)), INVALID),
     (dict(opts=_opts(pairs_n=2, tile_n=512)), INVALID),
+    (dict(opts=_opts(tile_n=512, cta_group=1)), UNSUPPORTED),   # the wide tile needs the CTA pair
+    (dict(ab=F16, cd=F16, opts=_opts(tile_n=512)), UNSUPPORTED),   # ... and a 32-bit accumulator
 ])
 def test_gemm_argument_errors(kw, want):
     assert _gemm(**kw) == want, tcx.lib().tcx_last_error()
@@ -78,6 +80,11 @@ def _sp(ab=F16, cd=F32, M=256, N=240, K=256, meta=P, opts=None):
     (dict(ab=S8, cd=F32, K=256), UNSUPPORTED),
     (dict(opts=_opts(pairs_m=2, tile_n=512)), INVALID),
     (dict(opts=_opts(tile_n=384)), INVALID),
+    (dict(opts=_opts(cta_group=3)), INVALID),        # as tcx_gemm_ex
+    (dict(opts=_opts(cta_group=-1)), INVALID),
+    (dict(opts=_opts(tile_n=512, cta_group=1)), UNSUPPORTED),   # the M-wide tile needs the CTA pair,
+    (dict(ab=S8, cd=S32, opts=_opts(tile_n=512)), UNSUPPORTED),  # a 16/32-bit kind
+    (dict(M=768, opts=_opts(tile_n=512)), UNSUPPORTED),          # and M % 512 == 0
     (dict(M=0), OK),
 ])
 def test_sparse_argument_errors(kw, want):
