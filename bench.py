@@ -351,17 +351,22 @@ def time_steps(work, steps, warmup, dist_on, sampler=None):
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st0 = torch.zeros(2 * 256, dtype=torch.int64, device=work.dev)
+    st1 = torch.zeros(2 * 256, dtype=torch.int64, device=work.dev)
     n0 = tcx.launch_count()
     t0 = time.time()
+    tcx.sm_clock_stamp(st0)                 # per-SM (clock64, globaltimer) just before / after the region
     e0.record(stream)
     for _ in range(steps):
         work.step()
     e1.record(stream)
+    tcx.sm_clock_stamp(st1)
     torch.cuda.synchronize()
     t1 = time.time()
     if dist_on:
         torch.distributed.barrier()
     launches = tcx.launch_count() - n0 + steps * getattr(work, "launches_per_step", 0)   # graph replays launch without the host counter
+    work.sm_mhz_eff = tcx.sm_mhz_between(st0, st1)
     return e0.elapsed_time(e1) / steps, launches, t0, t1
 
 
@@ -421,17 +426,43 @@ def best_of(work, n=10):
 
 def torch_matmul_anchor(work, steps):
     """same-run cuBLAS context for C3: torch.matmul on the bench's own bf16 A, B."""
+    return library_anchor(work, steps)
+
+
+def library_anchor(work, steps):
+    """the same-run library rate for this config's dtype and shape (cuBLAS through torch, no C):
+    bf16 torch.matmul, TF32 torch.matmul with allow_tf32 on the same TF32-representable FP32
+    operands, INT8 torch._int_mm (INT32 out).  A measured peak of that dtype on this box, beside
+    the bf16-peak x nominal-ratio denominator (the ratio alone let fracs pass 1)."""
     A, Bt = work.A, work.B.t()
-    for _ in range(3):
-        torch.matmul(A, Bt)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        torch.matmul(A, Bt)
-    e1.record()
-    torch.cuda.synchronize()
-    return round(work.flops / (e0.elapsed_time(e1) / steps * 1e-3) / 1e12, 1)
+    if work.kind == "s8":
+        fn = lambda: torch._int_mm(A, Bt)
+    elif work.kind == "tf32":
+        def fn():
+            prev = torch.backends.cuda.matmul.allow_tf32
+            torch.backends.cuda.matmul.allow_tf32 = True
+            try:
+                return torch.matmul(A, Bt)
+            finally:
+                torch.backends.cuda.matmul.allow_tf32 = prev
+    else:
+        fn = lambda: torch.matmul(A, Bt)
+    try:
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(max(3, steps)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return round(work.flops / (best * 1e-3) / 1e12, 1)
+    except Exception as e:   # a library without this dtype / shape: say so, never substitute
+        log("anchor unavailable:", e)
+        return None
 
 
 def tiles_steady_state(tcx, dev, count=524288, reps=10):
@@ -457,7 +488,8 @@ def tiles_steady_state(tcx, dev, count=524288, reps=10):
             "frac_of_hbm": round(gbs / peaks()["hbm"], 4)}
 
 
-def roofline(work, ms, pk, clocks=None):
+def roofline(work, ms, pk, clocks=None, anchor=None):
+    src = None
     if work.bound == "hbm":
         ach = work.alg_bytes / (ms * 1e-3) / 1e9
         peak = pk["hbm"]
@@ -466,6 +498,10 @@ def roofline(work, ms, pk, clocks=None):
         ach = work.flops / (ms * 1e-3) / 1e12
         peak = pk["bf16"] * KIND_RATIO[work.kind]
         unit = "TFLOP/s"
+        if anchor and anchor > peak:
+            # the same-run library kernel of this dtype beat the bf16 peak x nominal ratio: it is the
+            # higher measured rate of this dtype on this box, so it is the denominator
+            peak, src = anchor, "same-run library anchor (best of n, this dtype and shape)"
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -480,15 +516,23 @@ def roofline(work, ms, pk, clocks=None):
     if work.bound == "tensor":
         r = KIND_RATIO[work.kind]
         den = {"datasheet": {"peak": DATASHEET_BF16_TFLOPS * r, "frac": round(ach / (DATASHEET_BF16_TFLOPS * r), 4)}}
-        mhz = (clocks or {}).get("sm_mhz")
+        # the clock-normalised peak: the average SM clock over the timed region itself, from per-SM
+        # clock64 / globaltimer stamps bracketing it (tcx_sm_clock_stamp), else the NVML median
+        mhz_eff = getattr(work, "sm_mhz_eff", None)
+        mhz = mhz_eff or (clocks or {}).get("sm_mhz")
         if mhz:
             cn = 148 * BF16_FMA_PER_CLK_SM * r * 2 * mhz * 1e6 / 1e12
-            den["clock_normalised"] = {"peak": round(cn, 1), "sm_mhz": mhz, "frac": round(ach / cn, 4)}
+            den["clock_normalised"] = {"peak": round(cn, 1), "sm_mhz": round(mhz, 1), "frac": round(ach / cn, 4),
+                                       "clock_source": "in-run SM clock stamps" if mhz_eff else "NVML samples"}
+        if anchor:
+            den["same_run_library"] = {"peak": anchor, "frac": round(ach / anchor, 4)}
         extra["denominators"] = den
+    if src is None:
+        src = pk["source"] + (" x nominal %s/bf16 ratio %.1f" % (work.kind, KIND_RATIO[work.kind])
+                              if work.bound == "tensor" and KIND_RATIO[work.kind] != 1.0 else "")
     return {"bound": work.bound, "achieved": round(ach, 2), "peak": round(peak, 2), "unit": unit,
             "frac": round(ach / peak, 4), **extra, "traffic": traffic, "kernel": work.kernel,
-            "peak_source": pk["source"] + (" x nominal %s/bf16 ratio %.1f" % (work.kind, KIND_RATIO[work.kind])
-                                            if work.bound == "tensor" and KIND_RATIO[work.kind] != 1.0 else "")}
+            "peak_source": src}
 
 
 # ----------------------------------------------------------------------------------- oracle baseline
@@ -498,12 +542,14 @@ def oracle_sample(cfg, seconds=12.0, seed=0):
     import tcxgen as g
     cores = len(os.sched_getaffinity(0))
     rng = np.random.default_rng(seed)
+    wall0 = time.perf_counter()          # wall-clock cap: counter-based row generation is not timed
     if cfg in ("c3", "c3tf32", "c4"):
         M = N = K = 16384 if cfg == "c4" else 8192
         fmt = {"c3": "bf16", "c3tf32": "tf32", "c4": "s8"}[cfg]
         ab = {"bf16": O.BF16, "tf32": O.TF32, "s8": O.S8}[fmt]
-        # a sample of R rows x S cols of the same synthetic matrices (counter-based generator)
-        R, S = 16, 16
+        # a sample of R rows x S cols of the same synthetic matrices (counter-based generator; INT8's
+        # exact dot is cheap, so a bigger block keeps generation from dominating the wall time)
+        R, S = (64, 64) if cfg == "c4" else (16, 16)
 
         def rows_of(stream, idx, n_cols):
             out = []
@@ -516,7 +562,7 @@ def oracle_sample(cfg, seconds=12.0, seed=0):
 
         t_total = 0.0
         outputs = 0
-        while t_total < seconds:
+        while t_total < seconds and time.perf_counter() - wall0 < 2.5 * seconds + 2:
             ri = rng.integers(0, M, R); ci = rng.integers(0, N, S)
             Ah = rows_of(g.STREAM_A, ri, K)
             Bh = rows_of(g.STREAM_B, ci, K)
@@ -536,7 +582,7 @@ def oracle_sample(cfg, seconds=12.0, seed=0):
         M, N, K = 65536, 16384, 16384
         R, S = 8, 16
         t_total, outputs = 0.0, 0
-        while t_total < seconds:
+        while t_total < seconds and time.perf_counter() - wall0 < 2.5 * seconds + 2:
             ri = rng.integers(0, M, R); ci = rng.integers(0, N, S)
             vals = np.stack([_counter_row_fp(seed, g.STREAM_SPVAL, int(r), K // 2, "f16", redraw=True) for r in ri])
             meta = np.stack([_counter_meta_row(seed, int(r), K) for r in ri])
@@ -550,6 +596,50 @@ def oracle_sample(cfg, seconds=12.0, seed=0):
         return {"value": 2.0 * (K // 2) * outputs / t_total / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
                 "sample": f"{outputs} sampled outputs of the {M}x{N}x{K} 2:4 FP16 GEMM in {t_total:.1f} s",
                 "seconds": t_total}
+    if cfg == "c3f16acc":                        # FP16 A, B, FP16 C = 0, FP16 accumulator: exact, one RNE16
+        M = N = K = 8192
+        R, S = 16, 16
+        t_total, outputs = 0.0, 0
+        while t_total < seconds and time.perf_counter() - wall0 < 2.5 * seconds + 2:
+            ri = rng.integers(0, M, R); ci = rng.integers(0, N, S)
+            Ah = np.stack([_counter_row_fp(seed, g.STREAM_A, int(r), K, "f16") for r in ri])
+            Bh = np.stack([_counter_row_fp(seed, g.STREAM_B, int(c), K, "f16") for c in ci])
+            rr, cc = np.meshgrid(np.arange(R), np.arange(S), indexing="ij")
+            t0 = time.perf_counter()
+            O.gemm_samples(O.F16, Ah, Bh, np.zeros((R, S), np.uint16), rr.ravel(), cc.ravel(), cores, cd=O.F16)
+            t_total += time.perf_counter() - t0
+            outputs += R * S
+        return {"value": 2.0 * K * outputs / t_total / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                "sample": f"{outputs} sampled outputs of the {M}x{N}x{K} FP16-accumulate GEMM in {t_total:.1f} s",
+                "seconds": t_total}
+    if cfg in ("c4sp", "c3sptf32"):             # INT8 2:4 (C4's shape) / TF32 1:2 (C3's shape): expand, then dense
+        i8 = cfg == "c4sp"
+        M = N = K = 16384 if i8 else 8192
+        R, S = (32, 64) if i8 else (16, 16)
+        t_total, outputs = 0.0, 0
+        while t_total < seconds and time.perf_counter() - wall0 < 2.5 * seconds + 2:
+            ri = rng.integers(0, M, R); ci = rng.integers(0, N, S)
+            if i8:
+                v = np.stack([_counter_row_int32(seed, g.STREAM_SPVAL, int(r), K // 2, -128, 126) for r in ri])
+                vals = np.where(v >= 0, v + 1, v).astype(np.int8)
+                meta = np.stack([_counter_meta_row(seed, int(r), K) for r in ri])
+                Bh = np.stack([_counter_row_int8(seed, g.STREAM_B, int(c), K) for c in ci])
+                Ch = np.stack([_counter_row_int32(seed, g.STREAM_C, int(r), N)[ci] for r in ri]).astype(np.int32)
+            else:
+                vals = np.stack([_counter_row_fp(seed, g.STREAM_SPVAL, int(r), K // 2, "tf32", redraw=True) for r in ri])
+                meta = np.stack([_counter_meta_row_sp12(seed, int(r), K) for r in ri])
+                Bh = np.stack([_counter_row_fp(seed, g.STREAM_B, int(c), K, "tf32") for c in ci])
+                Ch = None
+            rr, cc = np.meshgrid(np.arange(R), np.arange(S), indexing="ij")
+            t0 = time.perf_counter()
+            dense = O.sp24_expand(vals, meta, K)
+            O.gemm_samples(O.S8 if i8 else O.TF32, dense, Bh, Ch.view(np.uint32) if Ch is not None else None,
+                           rr.ravel(), cc.ravel(), cores)
+            t_total += time.perf_counter() - t0
+            outputs += R * S
+        return {"value": 2.0 * (K // 2) * outputs / t_total / 1e12, "unit": "TOPS" if i8 else "TFLOP/s", "cores": cores,
+                "kind": "oracle", "sample": f"{outputs} sampled outputs of the {M}x{N}x{K} "
+                f"{'INT8 2:4' if i8 else 'TF32 1:2'} sparse GEMM in {t_total:.1f} s", "seconds": t_total}
     if cfg == "c1":
         count = 4096
         A = g.uniform_matrix((count, 16, 16), "f16", seed, g.STREAM_A)
@@ -591,12 +681,78 @@ def _counter_row_int32(seed, stream, r, n, lo=-(1 << 20), hi=1 << 20):
     return (torch.remainder(g._srl(z, 32), hi - lo + 1) + lo).to(torch.int32).numpy()
 
 
+def _counter_meta_row_sp12(seed, r, K):
+    """row r of tcxgen.sp12_problem_tf32's canonical metadata (pattern (z >> 32) mod 4 per group)"""
+    import tcxgen as g
+    G = K // 4
+    z = g.splitmix(seed, g.STREAM_POS, torch.arange(r * G, (r + 1) * G, dtype=torch.int64))
+    pat = torch.remainder(g._srl(z, 32), 4)
+    to_pair = torch.tensor([g.PAIRS.index((p & 1, 2 + (p >> 1))) for p in range(4)], dtype=torch.uint8)
+    return g.sp24_canonical_meta(to_pair[pat].view(1, G))[0].numpy().view(np.uint32)
+
+
 def _counter_meta_row(seed, r, K):
     import tcxgen as g
     G = K // 4
     z = g.splitmix(seed, g.STREAM_POS, torch.arange(r * G, (r + 1) * G, dtype=torch.int64))
     pairs = torch.remainder(g._srl(z, 32), 6).to(torch.uint8).view(1, G)
     return g.sp24_canonical_meta(pairs)[0].numpy().view(np.uint32)
+
+
+# ----------------------------------------------------------------------------------- multi-GPU
+def time_broadcast(t, dev, reps=3):
+    """the row-sharding layer's one data-path collective: NCCL broadcast of the
+    replicated operand B from rank 0, CUDA events on the current stream, max over ranks."""
+    import torch.distributed as dist
+    from paper_2206_02874_b200.dist import broadcast_replicated, max_over_ranks
+    broadcast_replicated(t, src=0)
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(reps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        broadcast_replicated(t, src=0)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, max_over_ranks(e0.elapsed_time(e1), dev))
+    nbytes = t.numel() * t.element_size()
+    return {"bytes": nbytes, "ms": round(best, 4), "algbw_GBs": round(nbytes / (best * 1e-3) / 1e9, 1)}
+
+
+def multi_gpu_extras(work, args, world, rank, dev, pk):
+    """N > 1: the broadcast of the headline config's B (bus rate and an end-to-end figure including
+    it), then strong-scaling lines for C4 and C5 — the configs north_star shards — each
+    rank its rows, max-over-ranks device time, whole-job value."""
+    from paper_2206_02874_b200.dist import max_over_ranks
+    out = {"broadcast": time_broadcast(work.B, dev)}
+    if work.bound == "tensor":
+        gemm_ms = max_over_ranks(time_steps(work, 3, 1, True)[0], dev)
+        tot = torch.tensor([work.flops], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tot)
+        out["with_broadcast"] = {"value": round(float(tot.item()) / ((gemm_ms + out["broadcast"]["ms"]) * 1e-3) / 1e12, 2),
+                                 "unit": work.unit, "note": "one GEMM step plus the one-time broadcast of B"}
+    if args.no_extras:
+        return out
+    for extra in ("c4", "c5"):
+        if extra == args.config:
+            continue
+        try:
+            w2 = Work(extra, rank, world, dev, scaling=args.scaling)
+            ms2, l2, _, _ = time_steps(w2, max(5, min(args.steps, 10)), 3, True)
+            ms2 = max_over_ranks(ms2, dev)
+            tot = torch.tensor([w2.flops], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tot)
+            out[extra] = {"value": round(float(tot.item()) / (ms2 * 1e-3) / 1e12, 3), "unit": w2.unit,
+                          "ms_per_step": round(ms2, 5), "rows_per_rank": int(w2.D.shape[0]),
+                          "scaling": "weak" if w2.weak else "strong",
+                          "broadcast": time_broadcast(w2.B, dev), "gpu_launches_rank0": l2}
+            del w2
+            torch.cuda.empty_cache()
+        except Exception as e:  # report, never hide
+            out[extra] = {"error": f"{type(e).__name__}: {e}"}
+    return out
 
 
 # ----------------------------------------------------------------------------------- main
@@ -606,8 +762,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="tcx", choices=["tcx", "reference"])
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                    help="N > 1: weak = every rank a full config-sized row block (default); strong = the config split by rows")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+                    help="N > 1: strong = the config split by rows (default: the SCALE ratio is then "
+                         "T1 / (N T_N)); weak = every rank a full config-sized row block")
     ap.add_argument("--sustained-s", type=float, default=4.0, help="seconds of the back-to-back sustained run (0 = skip)")
     ap.add_argument("--config", default="c3", choices=["c3", "c3tf32", "c4", "c5", "c1", "c4sp", "c3sptf32", "c3f16acc"])
     ap.add_argument("--no-extras", action="store_true")
@@ -660,12 +817,19 @@ def main():
     ms, launches, t0, t1 = time_steps(work, args.steps, args.warmup, dist_on)
     sampler.stop()
     clocks = sampler.summary(t0, t1)
+    if getattr(work, "sm_mhz_eff", None):
+        clocks["sm_mhz_in_run"] = round(work.sm_mhz_eff, 1)
     if dist_on:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    total_flops = work.flops * world
-    total_bytes = work.alg_bytes * world
+    # whole-job work: every rank's own FLOPs / bytes summed (uneven shards included), not world x
+    # this rank's
+    total_flops, total_bytes = work.flops, work.alg_bytes
+    if dist_on:
+        t = torch.tensor([work.flops, work.alg_bytes], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM)
+        total_flops, total_bytes = float(t[0].item()), float(t[1].item())
     value = (total_bytes / (ms * 1e-3) / 1e9) if work.unit == "GB/s" else total_flops / (ms * 1e-3) / 1e12
 
     e2e = None
@@ -676,12 +840,15 @@ def main():
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e2e_ms = float(t.item())
         ev = (total_bytes / (e2e_ms * 1e-3) / 1e9) if work.unit == "GB/s" else total_flops / (e2e_ms * 1e-3) / 1e12
-        e2e = {"value": round(ev, 3), "unit": work.unit, "h2d_bytes_per_step": work.h2d * world,
-               "d2h_bytes_per_step": work.d2h * world, "ms_per_step": round(e2e_ms, 4)}
+        io = torch.tensor([work.h2d, work.d2h], device=dev, dtype=torch.float64)
+        if dist_on:
+            torch.distributed.all_reduce(io, op=torch.distributed.ReduceOp.SUM)
+        e2e = {"value": round(ev, 3), "unit": work.unit, "h2d_bytes_per_step": int(io[0].item()),
+               "d2h_bytes_per_step": int(io[1].item()), "ms_per_step": round(e2e_ms, 4)}
 
     line = {"metric": metric, "value": round(value, 3), "unit": work.unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
-            "scaling": "weak" if (world == 1 or work.weak) else "strong",
+            "scaling": "weak" if work.weak else "strong",
             "vs_baseline": None,
             "dtype": {"c3": "bf16", "c3tf32": "tf32", "c4": "s8", "c5": "f16", "c1": "f16", "c4sp": "s8",
                       "c3sptf32": "tf32", "c3f16acc": "f16"}[args.config],
@@ -691,11 +858,17 @@ def main():
                                        if world > 1 else "single GPU"),
                        "l2": "inputs+outputs per step > 126 MiB L2 (no reuse across steps)" if args.config != "c1"
                        else "64 rotating batch copies (470 MB) > L2"},
-            "roofline": roofline(work, ms, pk, clocks), "clocks": clocks, "gpu_launches": launches,
+            "roofline": None, "clocks": clocks, "gpu_launches": launches,
             "e2e": e2e}
+    anchor = None
+    if rank == 0 and world == 1 and not args.no_extras and args.config in ("c3", "c3tf32", "c4"):
+        anchor = library_anchor(work, args.steps)
+    line["roofline"] = roofline(work, ms, pk, clocks, anchor)
+    if dist_on:
+        line["multi_gpu"] = multi_gpu_extras(work, args, world, rank, dev, pk)
     if rank == 0 and world == 1 and not args.no_extras and args.config == "c3":
         line["context"] = {"tcx_best_of_10_steps": best_of(work),
-                           "torch_matmul_bf16_tflops_same_run": torch_matmul_anchor(work, args.steps),
+                           "torch_matmul_bf16_tflops_same_run": anchor,
                            "note": "cuBLAS via torch.matmul(A, B^T) on the same bf16 A, B, bf16 output (no C): "
                                    "context only, not part of the step"}
         also = {}
@@ -710,12 +883,20 @@ def main():
                 sampler.stop()
                 v2 = w2.metric_value(ms2 * 1e-3)
                 ck2 = sampler.summary(u0, u1)
+                if getattr(w2, "sm_mhz_eff", None):
+                    ck2["sm_mhz_in_run"] = round(w2.sm_mhz_eff, 1)
+                anc = library_anchor(w2, 5) if extra in ("c3tf32", "c4") else None
                 also[extra] = {"workload": cfg_names[extra], "value": round(v2, 3), "unit": w2.unit,
-                               "ms_per_step": round(ms2, 5), "roofline": roofline(w2, ms2, pk, ck2), "gpu_launches": l2,
+                               "ms_per_step": round(ms2, 5), "roofline": roofline(w2, ms2, pk, ck2, anc), "gpu_launches": l2,
                                "clocks": ck2}
                 if extra == "c1":
                     also[extra]["steady_state"] = tiles_steady_state(w2.tcx, dev)
                 del w2
+                torch.cuda.empty_cache()
+                if not args.no_cpu_baseline:       # the oracle on the host cores, a bounded sample of this config
+                    cb2 = oracle_sample(extra, seconds=3.0)
+                    also[extra]["cpu_baseline"] = {k: (round(cb2[k], 9) if isinstance(cb2[k], float) else cb2[k])
+                                                   for k in ("value", "unit", "cores", "kind", "sample")}
                 torch.cuda.empty_cache()
             except Exception as e:  # report, never hide
                 also[extra] = {"error": f"{type(e).__name__}: {e}"}

@@ -250,7 +250,7 @@ typedef struct {
                         setting) */
   /* tcgen05 kinds only (0 / NULL = defaults): */
   int issuers;       /* issuing CTAs (CTA pairs for cta_group 2) per SM: 1 or 2 (0 = 1).  2 launches
-                        two CTAs on every SM and keeps those on SMs < num_sms */
+                        two CTAs on every SM of the chip (num_sms is then not used) */
   int n_acc;         /* distinct accumulators the ILP MMAs rotate over, 1 .. min(ILP, TMEM
                         columns / n) (0 = as many as fit, capped at ILP) */
   int mode;          /* tcx_probe_tc05_mode */
@@ -263,7 +263,14 @@ typedef struct {
                         Accumulator a has received (warmup_iters + iters) x |{i < ILP : i % n_acc
                         == a}| MMAs, the first with D = A.B (no C) */
 } tcx_probe_config;
-typedef enum { TCX_TC05_SYNC = 0, TCX_TC05_STREAM = 1, TCX_TC05_COMMIT = 2 } tcx_probe_tc05_mode;
+/* STREAM_ROT: STREAM with every MMA reading its operands from the next slot of a 4-stage smem ring
+ * at every 32/64-byte k-offset (a GEMM mainloop's smem read pattern; the fixed-address modes may be
+ * served from operand buffers).  STREAM_AREUSE: STREAM_ROT in pairs that share A through the
+ * A-operand collector (.collector::a::fill then ::lastuse, two accumulators: n_acc = 2, ILP even) —
+ * the N-wide tile's pattern, A read from smem once per pair.  Both: issuers = 1; the operand bytes
+ * are replicated into every slot, so the accumulator check of acc_out still holds. */
+typedef enum { TCX_TC05_SYNC = 0, TCX_TC05_STREAM = 1, TCX_TC05_COMMIT = 2, TCX_TC05_STREAM_ROT = 3,
+               TCX_TC05_STREAM_AREUSE = 4 } tcx_probe_tc05_mode;
 typedef struct {
   double cycles_per_iter_min, cycles_per_iter_median;
   double latency_cycles;          /* = cycles_per_iter_median */
@@ -308,6 +315,14 @@ tcx_status tcx_mma_tiles_tc05(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, i
  * ------------------------------------------------------------------------------------- */
 tcx_status tcx_mma_chain(tcx_dtype ab, int n_steps, int64_t count, const void* A0, const void* Bs, float* Ds,
                          void* stream);
+
+/* tcx_sm_clock_stamp — measurement helper (not part of the MMA path): one tiny grid of sm_count
+ * CTAs in stream order; the CTA(s) on SM s (%smid < max_sms) write d_out[2s] = clock64 and
+ * d_out[2s + 1] = %globaltimer (ns).  Two stamps bracketing a timed region give each SM's average
+ * clock over it, (dclock / dns) GHz — the clock-normalised peak's denominator, measured in the run
+ * itself rather than sampled by NVML.  d_out: device, 2 * max_sms int64 (caller-owned, 8-byte
+ * aligned).  SMs that received no CTA keep their previous contents.  Asynchronous. */
+tcx_status tcx_sm_clock_stamp(int64_t* d_out, int max_sms, void* stream);
 
 /* ------------------------------------------------------------------------------------- */
 const char* tcx_status_string(tcx_status s);

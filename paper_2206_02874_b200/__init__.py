@@ -33,7 +33,8 @@ _STATUS = {0: "TCX_OK", 1: "TCX_ERR_INVALID_VALUE", 2: "TCX_ERR_UNSUPPORTED", 3:
 EXPORTS = ["tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_mma_chain", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
            "tcx_sp24_meta_hw_bytes", "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_gemm_sp24_ex", "tcx_round_tf32",
            "tcx_probe", "tcx_ldmatrix_dump",
-           "tcx_status_string", "tcx_last_error", "tcx_version", "tcx_launch_count", "tcx_debug_trace"]
+           "tcx_status_string", "tcx_last_error", "tcx_version", "tcx_launch_count", "tcx_debug_trace",
+           "tcx_sm_clock_stamp"]
 
 
 class TcxError(RuntimeError):
@@ -94,9 +95,10 @@ def lib():
     L.tcx_version.restype = ctypes.c_char_p
     L.tcx_launch_count.restype = ctypes.c_uint64
     L.tcx_debug_trace.argtypes = [vp, i64]
+    L.tcx_sm_clock_stamp.argtypes = [vp, i32, vp]
     for f in ("tcx_mma_tiles", "tcx_mma_tiles_tc05", "tcx_mma_chain", "tcx_gemm", "tcx_gemm_ex", "tcx_sp24_compress",
               "tcx_sp24_pack_meta", "tcx_gemm_sp24", "tcx_gemm_sp24_ex", "tcx_round_tf32", "tcx_probe", "tcx_ldmatrix_dump",
-              "tcx_debug_trace"):
+              "tcx_debug_trace", "tcx_sm_clock_stamp"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -124,6 +126,24 @@ def _stream(t=None):
 
 def launch_count() -> int:
     return int(lib().tcx_launch_count())
+
+
+def sm_clock_stamp(buf):
+    """stamp (clock64, globaltimer) per SM into buf (int64 CUDA tensor of 2 * n_sm) in stream order"""
+    _dev_check(buf)
+    _need(buf.dtype == torch.int64 and buf.is_contiguous() and buf.numel() >= 2, "sm_clock_stamp: int64 buffer")
+    _check(lib().tcx_sm_clock_stamp(_ptr(buf), buf.numel() // 2, _stream(buf)))
+
+
+def sm_mhz_between(s0, s1):
+    """median over SMs of dclock64 / dglobaltimer between two stamp buffers (MHz); None if no SM has both"""
+    a = s0.view(-1, 2).cpu().double()
+    b = s1.view(-1, 2).cpu().double()
+    dc, dn = b[:, 0] - a[:, 0], b[:, 1] - a[:, 1]
+    ok = (dn > 0) & (dc > 0) & (a[:, 1] > 0)
+    if not bool(ok.any()):
+        return None
+    return float((dc[ok] / dn[ok]).median()) * 1000.0
 
 
 _TORCH_AB = {torch.float16: F16, torch.bfloat16: BF16, torch.int8: S8}
@@ -292,7 +312,8 @@ def sp24_pack_meta(meta_canon, M, K, ab=F16, check=True):
     return hw
 
 
-def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m=0, tf32=False, tile_m=0, pairs=(0, 0)):
+def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m=0, tf32=False, tile_m=0, pairs=(0, 0),
+              _knobs=0):
     """D = expand(vals, meta) x B + C; vals (M, K/2), B (N, K).  FP16/BF16 -> FP32, INT8 -> INT32
     (meta_hw packed with the same ab: sp24_pack_meta(meta, M, K, ab=S8) for int8)."""
     ab = ab_code(vals, tf32)
@@ -314,7 +335,7 @@ def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m
     _dev_check(vals, meta_hw, B, C, D)
     if D is None:
         D = torch.empty((M, N), dtype=_CD_TORCH[cd], device=vals.device)
-    opts = GemmOpts(cta_group, max_ctas, group_m, int(tile_m), pairs[0], pairs[1])
+    opts = GemmOpts(cta_group, max_ctas, group_m, int(tile_m), pairs[0], pairs[1], (ctypes.c_int * 2)(_knobs, 0))
     _check(lib().tcx_gemm_sp24_ex(ab, cd, M, N, K, _ptr(vals), vals.stride(0), _ptr(meta_hw), _ptr(B), B.stride(0),
                                   _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
                                   ctypes.byref(opts), _stream(vals)))
@@ -336,7 +357,7 @@ def round_tf32(x, out=None):
 # ---------------------------------------------------------------------------------------- probe
 PROBE_KINDS = {"mma_sync": 0, "mma_sp_sync": 1, "tc05": 2, "tc05_sp": 3, "ldmatrix": 4, "ld_shared": 5,
                "tmem_ld": 6, "tma_load": 7, "tc05_cp": 8, "tma_multicast": 9}
-TC05_MODES = {"sync": 0, "stream": 1, "commit": 2}
+TC05_MODES = {"sync": 0, "stream": 1, "commit": 2, "stream_rot": 3, "stream_areuse": 4}
 
 
 def probe(kind="mma_sync", ab=F16, cd=F32, m=16, n=8, k=16, cta_group=1, warps=1, ilp=1, iters=1024,

@@ -168,6 +168,15 @@ tcx_status tcx_debug_trace(void* d_buf, int64_t capacity) {
 }
 uint64_t tcx_launch_count(void) { return g_launches.load(); }
 
+tcx_status tcx_sm_clock_stamp(int64_t* d_out, int max_sms, void* stream) {
+  if (!d_out || max_sms < 1) return set_error(TCX_ERR_INVALID_VALUE, "tcx_sm_clock_stamp: NULL buffer / max_sms < 1");
+  if (((uintptr_t)d_out & 7u) != 0) return set_error(TCX_ERR_MISALIGNED, "tcx_sm_clock_stamp: buffer alignment");
+  DevInfo dev;
+  tcx_status st = current_device(&dev);
+  if (st != TCX_OK) return st;
+  return launch_sm_clock_stamp((long long*)d_out, max_sms, dev.sm_count, (cudaStream_t)stream);
+}
+
 tcx_status tcx_mma_tiles(tcx_dtype ab, tcx_dtype cd, int m, int n, int k, int64_t count, const void* A, const void* B,
                          const void* C, void* D, void* stream) {
   const bool fp = (ab == TCX_F16 || ab == TCX_BF16) && cd == TCX_F32 && m == 16 && n == 8 && (k == 16 || k == 8);
@@ -352,6 +361,9 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
                        "F16/BF16/TF32 and M %% 512 == 0");
     g.pairs_m = pm;
     g.pairs_n = pn;
+#if TCX_WATCHDOG
+    g.fault = opts->reserved[0];   // debug library: energy-decomposition knobs (gemm_sp24.cu)
+#endif
   }
   if (g.cta_group == 2 && M % 256)
     return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: the CTA-pair kernel needs M %% 256 == 0 (use cta_group=1)");

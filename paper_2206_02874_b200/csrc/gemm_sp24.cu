@@ -108,7 +108,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmC,
                  const __grid_constant__ CUtensorMap tmD, int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc,
-                 int group_m, uint64_t* trace, int64_t trace_cap) {
+                 int group_m, uint64_t* trace, int64_t trace_cap, int knobs) {
+  // knobs (debug library only, 0 in the product): energy decomposition of the pipeline —
+  // 2 = no MMAs (the MMA warp still waits and commits), 4 = no operand TMA loads (the producer only
+  // arrives), 8 = no epilogue global traffic (TMEM is still drained; C not loaded, D not stored)
+#if !TCX_WATCHDOG
+  knobs = 0;
+#endif
+  const bool k_nomma = knobs & 2, k_noload = knobs & 4, k_noepi = knobs & 8;
+  if (k_noepi) has_c = 0;
   using C_ = SpCfg<CG, KIND, MW>;
   constexpr int KL = C_::KL;
   constexpr int MH = C_::MH;
@@ -182,6 +190,11 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           uint8_t* se = sb + C_::B_BYTES;
           const int ka = (int)(kb * (KL / 2));     // kept-value column
           const int kx = (int)(kb * KL);           // logical column of B
+          if (k_noload) {                       // debug: the slot is "filled" without moving a byte
+            if (CG == 1 || leader) mbar_arrive_expect_tx(&sm->full[stage], 0);
+            if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&sm->full[stage], C_::STAGE_BYTES);
           } else {
@@ -219,6 +232,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       int acc = 0; uint32_t acc_phase = 0;
       // stage `st`, M-half h: metadata atoms -> TMEM (in order before the MMAs), then 4 sparse MMAs
       auto issue = [&](int st, int h, int64_t kb, uint32_t tmem_d) {
+        if (k_nomma) return;
         const uint32_t sa = smem_u32(smem + st * C_::STAGE_BYTES) + h * C_::A_HALF;
         const uint32_t sb = smem_u32(smem + st * C_::STAGE_BYTES) + C_::A_BYTES;
         const uint32_t se = sb + C_::B_BYTES + h * 2048 * C_::META_ATOMS;
@@ -420,7 +434,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
+        if (lane == 0 && !k_noepi) {
           int x, y; coords(q, x, y);
           tma_store_2d(&tmD, stg + b * 2048, x, y);
           bulk_commit();
@@ -504,7 +518,8 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   const uint32_t idesc = (1u << 2) | (cfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
                          ((uint32_t)((BM * CG) >> 4) << 24);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tE, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
-                                  a.C ? 1 : 0, idesc, a.group_m != 0 ? a.group_m : GROUP_M, a.trace, a.trace_cap));
+                                  a.C ? 1 : 0, idesc, a.group_m != 0 ? a.group_m : GROUP_M, a.trace, a.trace_cap,
+                                  a.fault));
   count_launch();
   return TCX_OK;
 }

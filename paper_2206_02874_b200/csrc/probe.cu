@@ -164,8 +164,8 @@ tcx_status launch_probe_mma(int ilp, int grid, int warps, int iters, long long* 
 //   COMMIT  ITERS x (commit -> wait) with no MMA: the commit round trip alone (latency split)
 // Operands (optional) are copied from global into the 128B-swizzled smem tiles the MMAs read; the
 // accumulators of one issuer (the first active one to finish) can be read back (acc_out) so a test can check the MMA count exactly.
-// Issuers whose SM (rank 0's %smid) is >= num_sms exit before touching TMEM (issuers = 2 launches
-// two CTAs per SM on every SM — the smem request caps residency at two — and keeps num_sms of them).
+// issuers = 2 launches two CTAs per SM on every SM (the smem request caps residency at two); %smid of
+// every CTA is recorded so the co-residency is checked, not assumed.
 struct Tc05ProbeArgs {
   int mode, iters, ilp, n_acc, acc_cols, alloc_cols, num_sms, a_bytes, b_bytes, n_rows;
   uint32_t idesc;
@@ -182,14 +182,16 @@ struct Tc05ProbeArgs {
 };
 constexpr int TC05_WARMUP = 2;
 constexpr int TC05_META_COLS = 8;
+constexpr int TC05_STAGES = 4;                  // rotating modes: stage buffers of A (16 KiB) + B (32 KiB)
+constexpr int TC05_STAGE_BYTES = 16384 + 32768;
 
 template <int CG, int KIND, bool SPARSE>
 __global__ void __launch_bounds__(128, 1)
 probe_tc05_kernel(const Tc05ProbeArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sa = smem;                 // 128 rows x 128 B (SW128)
-  uint8_t* sb = smem + 16384;         // up to 256 rows x 128 B (SW128)
+  uint8_t* sa = smem;                 // 128 rows x 128 B (SW128) per stage
+  uint8_t* sb = smem + 16384;         // up to 256 rows x 128 B (SW128) per stage
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base_s;
   __shared__ int smid_s;
@@ -206,33 +208,35 @@ probe_tc05_kernel(const Tc05ProbeArgs p) {
     asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(lead_smid) : "r"(a) : "memory");
   }
   const bool active = lead_smid < p.num_sms;
-  if (threadIdx.x == 0) {
-    p.smid_out[blockIdx.x] = active ? smid_s : -1;
-    if (p.num_sms < (1 << 30)) {
-      // issuers = 2: a gated CTA keeps its slot until every CTA of the grid is resident (the grid is
-      // two per SM, which the smem request makes the occupancy, so all are co-resident), so no
-      // later CTA is placed on an SM a gated one vacated
-      atomicAdd(p.arrive, 1);
-      while (*(volatile int*)p.arrive < (int)gridDim.x) __nanosleep(256);
-    }
-  }
+  if (threadIdx.x == 0) p.smid_out[blockIdx.x] = active ? smid_s : -1;
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();   // peer's smid read before anyone exits
   if (!active) return;
-  // operands: this CTA's A rows (rank * 128 ..) and B rows (rank * n_rows ..), SW128 placement
-  for (int i = threadIdx.x; i < (16384 + 32768) / 16; i += blockDim.x) ((uint4*)smem)[i] = make_uint4(0, 0, 0, 0);
+  // operands: this CTA's A rows (rank * 128 ..) and B rows (rank * n_rows ..), SW128 placement.  The
+  // rotating modes read TC05_STAGES stage buffers at every k-offset of the 128-byte row (like a GEMM
+  // ring): each row's operand bytes are replicated into every slot, so every MMA still computes the
+  // same A.B and the accumulator check holds
+  const bool rot = p.mode >= 3;
+  const int nst = rot ? TC05_STAGES : 1;
+  for (int i = threadIdx.x; i < nst * TC05_STAGE_BYTES / 16; i += blockDim.x) ((uint4*)smem)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
-  if (p.a_op) {
-    const int ch = p.a_bytes / 16;
-    for (int i = threadIdx.x; i < 128 * ch; i += blockDim.x) {
-      const int r = i / ch, c = i % ch;
-      *(uint4*)(sa + r * 128 + ((c ^ (r % 8)) * 16)) = *(const uint4*)(p.a_op + ((int64_t)rank * 128 + r) * p.a_bytes + c * 16);
+  for (int st = 0; st < nst; ++st) {
+    uint8_t* sa_s = sa + st * TC05_STAGE_BYTES;
+    uint8_t* sb_s = sb + st * TC05_STAGE_BYTES;
+    if (p.a_op) {
+      const int ch = p.a_bytes / 16, rep = rot ? 128 / p.a_bytes : 1;
+      for (int i = threadIdx.x; i < 128 * ch * rep; i += blockDim.x) {
+        const int r = i / (ch * rep), c = i % (ch * rep);
+        *(uint4*)(sa_s + r * 128 + ((c ^ (r % 8)) * 16)) =
+            *(const uint4*)(p.a_op + ((int64_t)rank * 128 + r) * p.a_bytes + (c % ch) * 16);
+      }
     }
-  }
-  if (p.b_op) {
-    const int ch = p.b_bytes / 16;
-    for (int i = threadIdx.x; i < p.n_rows * ch; i += blockDim.x) {
-      const int r = i / ch, c = i % ch;
-      *(uint4*)(sb + r * 128 + ((c ^ (r % 8)) * 16)) = *(const uint4*)(p.b_op + ((int64_t)rank * p.n_rows + r) * p.b_bytes + c * 16);
+    if (p.b_op) {
+      const int ch = p.b_bytes / 16, rep = rot ? 128 / p.b_bytes : 1;
+      for (int i = threadIdx.x; i < p.n_rows * ch * rep; i += blockDim.x) {
+        const int r = i / (ch * rep), c = i % (ch * rep);
+        *(uint4*)(sb_s + r * 128 + ((c ^ (r % 8)) * 16)) =
+            *(const uint4*)(p.b_op + ((int64_t)rank * p.n_rows + r) * p.b_bytes + (c % ch) * 16);
+      }
     }
   }
   fence_proxy_async_smem();
@@ -266,16 +270,51 @@ probe_tc05_kernel(const Tc05ProbeArgs p) {
     const int ilp = p.ilp, n_acc = p.n_acc;
     const uint32_t acc_step = (uint32_t)p.acc_cols;
     uint32_t phase = 0;
+    // rotating modes: MMA slot -> (stage, k-offset) of the operand ring.  The descriptors are
+    // advanced incrementally (start-address field in 16-byte units) so the issue loop stays a few
+    // uniform-register adds per MMA, as in a GEMM mainloop
+    const uint32_t a_adv = (uint32_t)p.a_bytes >> 4, b_adv = (uint32_t)p.b_bytes >> 4;
+    const int a_steps = 128 / p.a_bytes, b_steps = 128 / p.b_bytes;
+    constexpr uint32_t STAGE_ADV = TC05_STAGE_BYTES >> 4;
+    int j = 0, jb = 0, stg = 0;
+    uint64_t ra = ad, rb = bd;                       // current slot's descriptors
+    auto advance = [&]() {
+      if (++jb == b_steps) jb = 0;
+      if (++j == a_steps) { j = 0; jb = 0; if (++stg == TC05_STAGES) stg = 0; }
+      ra = ad + (uint64_t)(stg * STAGE_ADV + j * a_adv);
+      rb = bd + (uint64_t)(stg * STAGE_ADV + jb * b_adv);
+    };
     auto mma_iter = [&](uint32_t first) {
       if (elect_one()) {
         uint32_t d = tbase;
         int a = 0;
-        for (int i = 0; i < ilp; ++i) {
-          const uint32_t acc = (first && i < n_acc) ? 0u : 1u;   // first use of an accumulator: D = A.B
-          if constexpr (SPARSE) umma_sp<CG, KIND>(d, ad, bd, tmeta, p.idesc, acc);
-          else umma<CG, KIND>(d, ad, bd, p.idesc, acc);
-          d += acc_step;
-          if (++a == n_acc) { a = 0; d = tbase; }
+        if (p.mode == 4) {
+          // pairs sharing A through the collector: (acc 0, A fill, B of slot s), (acc 1, A lastuse,
+          // B of slot s + 1) — the N-wide tile's pattern; n_acc = 2
+          for (int i = 0; i + 1 < ilp; i += 2) {
+            const uint64_t a_d = ra, b0 = rb;
+            advance();
+            const uint64_t b1 = rb;
+            advance();
+            const uint32_t acc = first && i == 0 ? 0u : 1u;
+            if constexpr (SPARSE) {
+              umma_sp_c<CG, KIND, COLL_FILL>(tbase, a_d, b0, tmeta, p.idesc, acc);
+              umma_sp_c<CG, KIND, COLL_LASTUSE>(tbase + acc_step, a_d, b1, tmeta, p.idesc, acc);
+            } else {
+              umma_c<CG, KIND, COLL_FILL>(tbase, a_d, b0, p.idesc, acc);
+              umma_c<CG, KIND, COLL_LASTUSE>(tbase + acc_step, a_d, b1, p.idesc, acc);
+            }
+          }
+        } else {
+          for (int i = 0; i < ilp; ++i) {
+            const uint32_t acc = (first && i < n_acc) ? 0u : 1u;   // first use of an accumulator: D = A.B
+            const uint64_t a_d = p.mode == 3 ? ra : ad, b_d = p.mode == 3 ? rb : bd;
+            if (p.mode == 3) advance();
+            if constexpr (SPARSE) umma_sp<CG, KIND>(d, a_d, b_d, tmeta, p.idesc, acc);
+            else umma<CG, KIND>(d, a_d, b_d, p.idesc, acc);
+            d += acc_step;
+            if (++a == n_acc) { a = 0; d = tbase; }
+          }
         }
       }
       __syncwarp();
@@ -294,13 +333,14 @@ probe_tc05_kernel(const Tc05ProbeArgs p) {
       tc05_fence_after();
     };
     const bool mmas = p.mode != 2;
+    const bool stream = p.mode == 1 || p.mode >= 3;
     for (int it = 0; it < TC05_WARMUP; ++it) {
       if (mmas) mma_iter(it == 0);
       commit_wait();
     }
     const long long t0 = clock64();
     const uint64_t g0 = globaltimer();
-    if (p.mode == 1) {
+    if (stream) {
       for (int it = 0; it < p.iters; ++it) mma_iter(0);
       commit_wait();
     } else {
@@ -353,7 +393,7 @@ template <int CG, int KIND, bool SPARSE>
 tcx_status launch_probe_tc05(int grid_ctas, int issuers, const Tc05ProbeArgs& a) {
   auto kern = probe_tc05_kernel<CG, KIND, SPARSE>;
   // 49 KiB of operands; two issuers per SM: request enough smem that at most two CTAs fit an SM
-  const int smem = issuers == 2 ? 100 * 1024 : 16384 + 32768 + 1024;
+  const int smem = a.mode >= 3 ? TC05_STAGES * TC05_STAGE_BYTES + 1024 : issuers == 2 ? 100 * 1024 : TC05_STAGE_BYTES + 1024;
   TCX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid_ctas);
@@ -572,7 +612,11 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
     const int kexp = kbytes / esz;
     if (k != kexp) { st = set_error(TCX_ERR_UNSUPPORTED, "tcx_probe: tcgen05 K must be %d for this kind", kexp); goto done; }
     if (issuers != 1 && issuers != 2) { st = set_error(TCX_ERR_INVALID_VALUE, "tcx_probe: issuers must be 1 or 2"); goto done; }
-    if (mode < 0 || mode > 2) { st = set_error(TCX_ERR_INVALID_VALUE, "tcx_probe: tcgen05 mode must be 0, 1 or 2"); goto done; }
+    if (mode < 0 || mode > 4) { st = set_error(TCX_ERR_INVALID_VALUE, "tcx_probe: tcgen05 mode must be 0 .. 4"); goto done; }
+    if (mode >= 3 && issuers != 1) { st = set_error(TCX_ERR_UNSUPPORTED, "tcx_probe: rotating modes need issuers = 1"); goto done; }
+    if (mode == 4 && (cfg->n_acc != 2 || ilp % 2)) {
+      st = set_error(TCX_ERR_INVALID_VALUE, "tcx_probe: STREAM_AREUSE needs n_acc = 2 and an even ILP"); goto done;
+    }
     const bool mok = cg == 1 ? (m == 64 || m == 128) : (m == 128 || m == 256);
     const bool nok = n >= 16 && n <= 256 && n % 16 == 0;
     if (!mok || !nok) { st = set_error(TCX_ERR_UNSUPPORTED, "tcx_probe: tcgen05 M/N"); goto done; }
@@ -590,15 +634,16 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
     const uint32_t cfmt = ab == TCX_S8 ? 2u : 1u;
     const uint32_t idesc = (sp ? (1u << 2) : 0u) | (cfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(n >> 3) << 17) |
                            ((uint32_t)(m >> 4) << 24);
-    // issuers = 1: num_sms CTAs (pairs), one per SM; issuers = 2: two CTAs on every SM, the clusters
-    // whose leader sits on SM >= num_sms exit at once
+    // issuers = 1: num_sms CTAs (pairs), one per SM; issuers = 2: two CTAs on every SM of the chip
+    // (the smem request caps residency at two; num_sms is not used — which SM a CTA lands on cannot
+    // be chosen, and gating by %smid lets the scheduler refill vacated SMs)
     const int grid = issuers == 1 ? std::max(1, nsm / cg) * cg : dev.sm_count * 2;
     const int nclusters = grid / cg;
     int* d_smid = nullptr;
     TCX_CUDA_TRY(cudaMalloc(&d_smid, (grid + 2) * sizeof(int)));
     long long* d_t = nullptr;              // cycles, ns, g0, g1 per issuer
     TCX_CUDA_TRY(cudaMalloc(&d_t, 4 * nclusters * sizeof(long long)));
-    Tc05ProbeArgs pa{mode, iters, ilp, n_acc, n, alloc_cols, issuers == 1 ? 1 << 30 : nsm, 32, kbytes, n / cg, idesc,
+    Tc05ProbeArgs pa{mode, iters, ilp, n_acc, n, alloc_cols, 1 << 30, 32, kbytes, n / cg, idesc,
                      (const uint8_t*)cfg->a_op, (const uint8_t*)cfg->b_op, d_t, d_t + nclusters,
                      d_smid, (uint32_t*)cfg->acc_out, d_smid + grid, d_smid + grid + 1, d_t + 2 * nclusters,
                      d_t + 3 * nclusters};
@@ -701,4 +746,26 @@ done:
   return st;
 }
 
+}  // namespace tcx
+
+// ------------------------------------------------------------------ SM clock stamps (tcx_sm_clock_stamp)
+namespace tcx {
+namespace {
+__global__ void sm_clock_stamp_kernel(long long* out, int max_sms) {
+  int sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  const long long c = clock64();
+  const uint64_t g = globaltimer();
+  if (sm < max_sms) {
+    // one record per SM; a second CTA on the same SM overwrites it with its own consistent pair
+    out[2 * sm] = c;
+    out[2 * sm + 1] = (long long)g;
+  }
+}
+}  // namespace
+
+tcx_status launch_sm_clock_stamp(long long* out, int max_sms, int sm_count, cudaStream_t s) {
+  sm_clock_stamp_kernel<<<sm_count, 32, 0, s>>>(out, max_sms);
+  TCX_CUDA_TRY(cudaGetLastError());
+  return TCX_OK;
+}
 }  // namespace tcx

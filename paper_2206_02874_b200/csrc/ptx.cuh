@@ -276,6 +276,58 @@ __device__ __forceinline__ void umma_sp(uint32_t tmem_d, uint64_t adesc, uint64_
 #undef TCX_UMMA_SP
 }
 
+// A-operand collector usage (tcgen05.mma .collector::a::*): FILL keeps this MMA's A in the collector
+// buffer, USE / LASTUSE read it from there instead of shared memory (LASTUSE releases it) — two MMAs
+// that share A (different B / accumulator) read A from smem once
+enum : int { COLL_NONE = 0, COLL_FILL = 1, COLL_USE = 2, COLL_LASTUSE = 3 };
+template <int CG, int KIND, int COLL>
+__device__ __forceinline__ void umma_c(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  if constexpr (COLL == COLL_NONE) { umma<CG, KIND>(tmem_d, adesc, bdesc, idesc, accumulate); return; }
+#define TCX_UMMA_C(CGS, KS, CS)                                                                       \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                                   \
+               "tcgen05.mma.cta_group::" CGS ".kind::" KS ".collector::a::" CS " [%0], %1, %2, %3, p;\n\t}" \
+               :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory")
+#define TCX_UMMA_C_K(CGS, CS)                                     \
+  if constexpr (KIND == KIND_F16) TCX_UMMA_C(CGS, "f16", CS);      \
+  else if constexpr (KIND == KIND_TF32) TCX_UMMA_C(CGS, "tf32", CS); \
+  else TCX_UMMA_C(CGS, "i8", CS);
+  if constexpr (CG == 1) {
+    if constexpr (COLL == COLL_FILL) { TCX_UMMA_C_K("1", "fill") }
+    else if constexpr (COLL == COLL_USE) { TCX_UMMA_C_K("1", "use") }
+    else { TCX_UMMA_C_K("1", "lastuse") }
+  } else {
+    if constexpr (COLL == COLL_FILL) { TCX_UMMA_C_K("2", "fill") }
+    else if constexpr (COLL == COLL_USE) { TCX_UMMA_C_K("2", "use") }
+    else { TCX_UMMA_C_K("2", "lastuse") }
+  }
+#undef TCX_UMMA_C_K
+#undef TCX_UMMA_C
+}
+template <int CG, int KIND, int COLL>
+__device__ __forceinline__ void umma_sp_c(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t tmem_e, uint32_t idesc,
+                                          uint32_t accumulate) {
+  if constexpr (COLL == COLL_NONE) { umma_sp<CG, KIND>(tmem_d, adesc, bdesc, tmem_e, idesc, accumulate); return; }
+#define TCX_UMMA_SPC(CGS, KS, CS)                                                                          \
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"                                        \
+               "tcgen05.mma.sp.cta_group::" CGS ".kind::" KS ".collector::a::" CS " [%0], %1, %2, [%3], %4, p;\n\t}" \
+               :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(tmem_e), "r"(idesc), "r"(accumulate) : "memory")
+#define TCX_UMMA_SPC_K(CGS, CS)                                       \
+  if constexpr (KIND == KIND_F16) TCX_UMMA_SPC(CGS, "f16", CS);        \
+  else if constexpr (KIND == KIND_TF32) TCX_UMMA_SPC(CGS, "tf32", CS); \
+  else TCX_UMMA_SPC(CGS, "i8", CS);
+  if constexpr (CG == 1) {
+    if constexpr (COLL == COLL_FILL) { TCX_UMMA_SPC_K("1", "fill") }
+    else if constexpr (COLL == COLL_USE) { TCX_UMMA_SPC_K("1", "use") }
+    else { TCX_UMMA_SPC_K("1", "lastuse") }
+  } else {
+    if constexpr (COLL == COLL_FILL) { TCX_UMMA_SPC_K("2", "fill") }
+    else if constexpr (COLL == COLL_USE) { TCX_UMMA_SPC_K("2", "use") }
+    else { TCX_UMMA_SPC_K("2", "lastuse") }
+  }
+#undef TCX_UMMA_SPC_K
+#undef TCX_UMMA_SPC
+}
+
 // smem -> TMEM copy, 128 lanes x 128 bits
 template <int CG>
 __device__ __forceinline__ void tc05_cp_128x128b(uint32_t tmem_addr, uint64_t sdesc_) {

@@ -72,6 +72,7 @@ tcx_status launch_sp24_pack(tcx_dtype ab, int64_t M, int64_t K, const uint32_t* 
                             cudaStream_t s);
 tcx_status launch_round_tf32(const float* in, float* out, int64_t n, cudaStream_t s);
 tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_result* out);
+tcx_status launch_sm_clock_stamp(long long* out, int max_sms, int sm_count, cudaStream_t s);
 tcx_status run_probe_mem(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_result* out);
 tcx_status launch_ldmatrix_dump(int n, int trans, const void* src, const int* row_elem, uint32_t* out, cudaStream_t s);
 

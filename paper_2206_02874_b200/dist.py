@@ -49,14 +49,21 @@ def broadcast_replicated(t: torch.Tensor, src: int = 0, group=None) -> torch.Ten
     return t
 
 
-def gather_rows(local: torch.Tensor, M: int, group=None) -> torch.Tensor:
-    """verification only: all-gather the row shards of D into the full M x N matrix."""
+def gather_rows(local: torch.Tensor, M: int | None = None, group=None) -> torch.Tensor:
+    """verification only: all-gather every rank's row block of D, in rank order, into one matrix.
+    The block sizes are exchanged first, so any shard plan works (strong: the M x N matrix; weak:
+    the world x M-row problem); M, if given, is checked against the gathered row count."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return local
     rank = dist.get_rank(group)
     N = local.shape[1]
-    sizes = [row_shard(M, world, r)[1] - row_shard(M, world, r)[0] for r in range(world)]
+    mine = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
+    all_sizes = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(all_sizes, mine, group=group)
+    sizes = [int(t.item()) for t in all_sizes]
+    if M is not None and sum(sizes) != M:
+        raise ValueError(f"gather_rows: shards hold {sum(sizes)} rows, expected {M}")
     maxr = max(sizes)
     pad = torch.zeros(maxr, N, dtype=local.dtype, device=local.device)
     pad[: sizes[rank]] = local

@@ -60,6 +60,54 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _strong_worker(rank, world, port, q):
+    """bench.py's default multi-GPU mode (strong scaling): the config's rows split by shard_plan,
+    uneven when the 256-row blocks do not divide evenly; whole-job work = SUM over ranks of each
+    rank's own FLOPs (not world x this rank's), time = MAX over ranks; weak shards gather too."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        M, N, K = 1280, 32, 48                     # 5 blocks of 256 rows over 2 ranks: 512 + 768
+        g = torch.Generator().manual_seed(11)
+        A = torch.randn(M, K, generator=g, dtype=torch.float64)
+        B = torch.randn(N, K, generator=g, dtype=torch.float64) if rank == 0 else torch.zeros(N, K, dtype=torch.float64)
+        tdist.broadcast_replicated(B, src=0)
+        m0, m1, seed, total = tdist.shard_plan(M, world, rank, "strong")
+        local = lambda a, b, c, d, **kw: a @ b.T
+        Dl = tdist.sharded_gemm(A[m0:m1], B, local_fn=local)
+        flops = torch.tensor([2.0 * (m1 - m0) * N * K], dtype=torch.float64)
+        dist.all_reduce(flops, op=dist.ReduceOp.SUM)
+        D = tdist.gather_rows(Dl, M)
+        ok = torch.equal(D, A @ B.T) and float(flops.item()) == 2.0 * M * N * K and total == M
+        # weak plan: each rank a full M-row block of its own; gather_rows stacks them in rank order
+        w0, w1, wseed, wtotal = tdist.shard_plan(M, world, rank, "weak")
+        Aw = torch.randn(M, K, generator=torch.Generator().manual_seed(wseed), dtype=torch.float64)
+        Dw = tdist.gather_rows(Aw @ B.T, wtotal)
+        ref = torch.cat([torch.randn(M, K, generator=torch.Generator().manual_seed(tdist.shard_plan(M, world, r, "weak")[2]),
+                                     dtype=torch.float64) for r in range(world)]) @ B.T
+        ok = ok and torch.equal(Dw, ref) and (w0, w1) == (0, M)
+        q.put((rank, ok, m1 - m0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(120)
+def test_gloo_world2_strong_plan_uneven_shards():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_strong_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=90) for _ in range(world))
+    for p in ps:
+        p.join(timeout=30)
+    assert all(ok for _, ok, _ in res), res
+    assert [rows for _, _, rows in res] == [512, 768]
+
+
 @pytest.mark.timeout(120)
 def test_gloo_world2_broadcast_shard_gather():
     world = 2

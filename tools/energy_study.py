@@ -74,6 +74,10 @@ def variant(name):
         if "pm2" in name:
             kw["tile_m"] = 256
             kw["pairs"] = (2, 1)
+        # debug library (TCX_LIB_PATH=libtcx_debug.so) decomposition knobs: _nomma, _noload, _noepi
+        kn = (2 if "_nomma" in name else 0) | (4 if "_noload" in name else 0) | (8 if "_noepi" in name else 0)
+        if kn:
+            kw["_knobs"] = kn
         return (lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, C, w.D, **kw)), w.flops
     if name.startswith("c3") or name.startswith("c4"):
         w = work(name[:2])
@@ -84,13 +88,41 @@ def variant(name):
         kw = {"tile_n": 512} if "w512" in name else {}
         return (lambda: tcx.gemm(w.A, w.B, C, w.D, **kw)), w.flops
     if name.startswith("probe"):
-        sp = name == "probe_sp"
+        # probe_{sp,bf16}[_rot|_areuse]: pure MMA streams on every SM (smem-resident operands); _rot reads
+        # a 4-stage ring at every k-offset (a GEMM's smem read pattern), _areuse shares A via the collector
+        # suffix _n: operands drawn N(0,1) (the GEMM configs' data) instead of {-1, 0, 1}
+        sp = name.startswith("probe_sp")
+        base = name[:-2] if name.endswith("_n") else name
+        mode = "stream_areuse" if base.endswith("_areuse") else "stream_rot" if base.endswith("_rot") else "stream"
         ab = tcx.F16 if sp else tcx.BF16
         n, k = (240, 32) if sp else (256, 16)
         iters = 4096
+        es = 2
+        fmt = "f16" if sp else "bf16"
+        if name.endswith("_n"):
+            a_op = g.normal_matrix((256, 32 // es), fmt, 1, 1, "cuda", redraw_zero=sp)
+            b_op = g.normal_matrix((n, (64 if sp else 32) // es), fmt, 1, 2, "cuda")
+        else:
+            a_op = g.int32_matrix((256, 32 // es), 1, 1, -1, 1, "cuda").to(torch.float16 if sp else torch.bfloat16)
+            b_op = g.int32_matrix((n, (64 if sp else 32) // es), 1, 2, -1, 1, "cuda").to(a_op.dtype)
         fl = 2.0 * 74 * iters * 16 * 256 * n * k
         return (lambda: tcx.probe("tc05_sp" if sp else "tc05", ab, tcx.F32, 256, n, k, cta_group=2, ilp=16,
-                                  iters=iters, repeats=1, num_sms=148, n_acc=1, mode="stream")), fl
+                                  iters=iters, repeats=1, num_sms=148, n_acc=2 if mode == "stream_areuse" else 1,
+                                  mode=mode, a_op=a_op, b_op=b_op)), fl
+    if name == "tma_l2":
+        # L2 -> SM operand staging alone: every SM streams 8 x 16 KiB TMA boxes per wait from an
+        # L2-resident 16 MiB source (tcx_probe TMA_LOAD); "flops" here = bytes delivered
+        iters = 20000
+        return (lambda: tcx.probe("tma_load", tcx.S8, tcx.S32, 128, 128, 0, ilp=8, iters=iters, repeats=1,
+                                  num_sms=148)), float(148 * (iters + 4) * 8 * 128 * 128)
+    if name == "dram_copy":
+        # HBM alone: a 2 GiB random buffer copied (read + write bytes), far beyond L2
+        if "dram" not in WORK:
+            WORK.clear(); torch.cuda.empty_cache()
+            a = torch.randint(-2 ** 31, 2 ** 31 - 1, (1 << 29,), dtype=torch.int32, device="cuda")
+            WORK["dram"] = (a, torch.empty_like(a))
+        a, b = WORK["dram"]
+        return (lambda: b.copy_(a)), float(2 * a.numel() * 4)
     if name == "idle":
         return (lambda: time.sleep(0.05)), 0.0
     raise ValueError(name)
@@ -136,6 +168,7 @@ def measure(name, seconds, nv):
             "J_per_launch": round(joules / n, 4), "W": round(joules / (t1 - t0), 1),
             "tflops": round(flops / (ms * 1e-3) / 1e12, 1) if flops else None,
             "pJ_per_flop": round(joules / n / flops * 1e12, 4) if flops else None,
+            "note": "tma_l2 / dram_copy: 'tflops' and 'pJ_per_flop' are per BYTE moved" if name in ("tma_l2", "dram_copy") else None,
             "sm_mhz_median": mhz[len(mhz) // 2] if mhz else None,
             "power_cap_frac": round(sum(1 for x in s if x[1] & 4) / max(1, len(s)), 2)}
 
