@@ -354,8 +354,8 @@ tcx_status tcx_gemm_sp24_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, in
     const int pm = opts->pairs_m ? opts->pairs_m : 1, pn = opts->pairs_n ? opts->pairs_n : 1;
     if (pm < 1 || pm > 2 || pn < 1 || pn > 2)
       return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm_sp24: pairs_m and pairs_n must be 0, 1 or 2");
-    if ((pm > 1 || pn > 1) && (g.cta_group != 2 || g.tile_n == 512))
-      return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm_sp24: multicast groups need cta_group 2 and the 256-row tile");
+    if ((pm > 1 || pn > 1) && g.cta_group != 2)
+      return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm_sp24: multicast groups need cta_group 2");
     if (g.tile_n == 512 && (g.cta_group != 2 || ab == TCX_S8 || M % 512))
       return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm_sp24: tile_n 512 (the 512 x 240 pair tile) needs cta_group 2, "
                        "F16/BF16/TF32 and M %% 512 == 0");

@@ -111,6 +111,35 @@ __device__ __forceinline__ void tile_coords(int64_t tile, int64_t m_tiles, int64
   nt = by_m ? b : a;
 }
 
+#if TCX_WATCHDOG
+// debug library, energy decomposition (knob "no operand loads"): fill the operand ring once with
+// pseudo-random FP16/BF16 values of N(0,1)-like magnitude (random sign, exponent 2^-4 .. 2^1, random
+// fraction) and valid 2:4 metadata nibbles, so the MMAs of a load-free run toggle like real data
+__device__ __forceinline__ uint32_t dbg_hash(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16; return x;
+}
+__device__ __forceinline__ uint32_t dbg_half(uint32_t h, bool bf16) {
+  const uint32_t sign = (h >> 31) & 1u, e = 11u + (h >> 28 & 7u) % 6u;     // f16 exponent field 11..16
+  if (!bf16) return (sign << 15) | (e << 10) | (h & 0x3FFu);
+  return (sign << 15) | ((e - 15u + 127u) << 7) | (h & 0x7Fu);
+}
+__device__ void dbg_fill_ring(uint8_t* base, int bytes, int meta_off, int meta_bytes, int stage_bytes, bool bf16) {
+  static const uint8_t nib[6] = {0x4, 0x8, 0xC, 0x9, 0xD, 0xE};
+  for (int i = threadIdx.x * 4; i < bytes; i += blockDim.x * 4) {
+    const uint32_t h = dbg_hash((uint32_t)i * 2654435761u + blockIdx.x * 97u);
+    const int in_stage = i % stage_bytes;
+    uint32_t w;
+    if (meta_bytes > 0 && in_stage >= meta_off && in_stage < meta_off + meta_bytes) {
+      w = 0;
+      for (int j = 0; j < 8; ++j) w |= (uint32_t)nib[(h >> (4 * j)) % 6u] << (4 * j);
+    } else {
+      w = dbg_half(h, bf16) | (dbg_half(dbg_hash(h), bf16) << 16);
+    }
+    *(uint32_t*)(base + i) = w;
+  }
+}
+#endif
+
 template <int CG, int KIND, int NH, int PM, int PN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -121,6 +150,13 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem* sm = (Smem*)(smem + C_::SMEM_DATA + C_::STG_BYTES);
+  // `fault` (debug library only, 0 in the product): 1 = drop one TMA load (watchdog test); energy
+  // decomposition bits as in gemm_sp24.cu: 2 = no MMAs, 4 = no operand loads, 8 = no epilogue traffic
+#if !TCX_WATCHDOG
+  fault = 0;
+#endif
+  const bool k_nomma = fault & 2, k_noload = fault & 4, k_noepi = fault & 8;
+  if (k_noepi && KIND != KIND_F16ACC) has_c = 0;
 
   constexpr int P = PM * PN;                 // CTA pairs per cluster
   constexpr int CL = CG * P;                 // CTAs per cluster
@@ -170,6 +206,13 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   // grid's tail; no global memory is touched before its completion
   pdl_wait();
   pdl_trigger();
+#if TCX_WATCHDOG
+  if (k_noload && KIND == KIND_F16) {
+    dbg_fill_ring(smem, C_::SMEM_DATA, 0, 0, C_::STAGE_BYTES, true);
+    fence_proxy_async_smem();
+    __syncthreads();
+  }
+#endif
 
   if (warp == 0) {
     // ================= TMA producer =================
@@ -190,6 +233,11 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           uint8_t* sa = smem + stage * C_::STAGE_BYTES;
           uint8_t* sb = sa + C_::A_BYTES;
           const int kx = (int)(kb * (KBYTES / KindT<KIND>::ESIZE));
+          if (k_noload) {                       // debug: the slot is "filled" without moving a byte
+            if (CG == 1 || leader) mbar_arrive_expect_tx(&sm->full[stage], 0);
+            if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&sm->full[stage], C_::STAGE_BYTES);
             tma_load_2d(sa, &tmA, &sm->full[stage], kx, arow);
@@ -200,7 +248,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
 #if TCX_WATCHDOG
             // fault injection (debug library): the first A load is never issued, its barrier never
             // completes, and the MMA warp's bounded wait traps
-            if (fault == 1 && tile == cluster_id && kb == 0) {
+            if ((fault & 1) && tile == cluster_id && kb == 0) {
               if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
               continue;
             }
@@ -235,6 +283,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       // FP16 accumulate with C: the accumulator holds C (preloaded) from the first MMA on
       const bool acc16_c = KIND == KIND_F16ACC && has_c;
       auto issue = [&](int st, int h, int64_t kb, uint32_t tmem_d) {
+        if (k_nomma) return;
         const uint32_t sa = smem_u32(smem + st * C_::STAGE_BYTES);
         const uint32_t sb = sa + C_::A_BYTES + h * C_::HALF_BYTES;              // N-half h's B rows
 #pragma unroll
@@ -294,7 +343,25 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           tc05_fence_after();
           if (elect_one()) {
 #pragma unroll
-            for (int h = 0; h < NH; ++h) issue(stage, h, kb, tmem_d);
+            if constexpr (NH == 2 && KIND != KIND_F16ACC) {
+              // both N-halves read the same A: per k-step the half-0 MMA fills the A-operand collector
+              // and the half-1 MMA reuses it (A read from smem once per pair of MMAs); each
+              // accumulator still sees its k-steps in ascending order, so the result is unchanged
+              if (!k_nomma) {
+                const uint32_t sa = smem_u32(smem + stage * C_::STAGE_BYTES);
+                const uint32_t sb0 = sa + C_::A_BYTES, sb1 = sb0 + C_::HALF_BYTES;
+#pragma unroll
+                for (int k = 0; k < KBYTES / UMMA_KBYTES; ++k) {
+                  const uint64_t ad = sdesc(sa + k * UMMA_KBYTES, 16, 1024, 2);
+                  const uint32_t en = (kb | k) ? 1u : 0u;
+                  umma_c<CG, KIND, COLL_FILL>(tmem_d, ad, sdesc(sb0 + k * UMMA_KBYTES, 16, 1024, 2), idesc, en);
+                  umma_c<CG, KIND, COLL_LASTUSE>(tmem_d + BN, ad, sdesc(sb1 + k * UMMA_KBYTES, 16, 1024, 2), idesc, en);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int h = 0; h < NH; ++h) issue(stage, h, kb, tmem_d);
+            }
             commit_slot(&sm->empty[stage]);                       // frees the smem slot
             if (kb == k_blocks - 1) commit_acc(&sm->tmem_full[acc]);   // accumulator ready
 #if TCX_WATCHDOG
@@ -566,7 +633,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         fence_proxy_async_smem();
         __syncwarp();
         TCX_STAMP(it, ch, 4);
-        if (lane == 0) {
+        if (lane == 0 && !k_noepi) {
           int x, y; coords(q, x, y);
           tma_store_2d(&tmD, buf, x, y);
           bulk_commit();

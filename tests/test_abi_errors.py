@@ -78,7 +78,8 @@ def _sp(ab=F16, cd=F32, M=256, N=240, K=256, meta=P, opts=None):
     (dict(meta=P + 4), MISALIGNED),
     (dict(M=128), UNSUPPORTED),                      # the CTA pair needs M % 256
     (dict(ab=S8, cd=F32, K=256), UNSUPPORTED),
-    (dict(opts=_opts(pairs_m=2, tile_n=512)), INVALID),
+    (dict(opts=_opts(pairs_m=2, cta_group=1)), INVALID),       # multicast groups need the CTA pair
+    (dict(M=256, opts=_opts(pairs_m=2, tile_n=512)), UNSUPPORTED),   # M-wide needs M % 512
     (dict(opts=_opts(tile_n=384)), INVALID),
     (dict(opts=_opts(cta_group=3)), INVALID),        # as tcx_gemm_ex
     (dict(opts=_opts(cta_group=-1)), INVALID),

@@ -239,13 +239,36 @@ def test_sparse_multicast_groups_vs_oracle_and_default(shape, pairs):
     fp_bound_check(host_bits(Dm).ravel(), ref, absv, K, f"sp24 mc {shape} {pairs}")
 
 
+@pytest.mark.parametrize("pairs", [(2, 1), (1, 2), (2, 2)])
+@pytest.mark.parametrize("shape", [(512, 240, 128), (1536, 496, 640), (2560, 1008, 256)])
+def test_sparse_mwide_multicast_groups_vs_oracle(shape, pairs):
+    """the 512 x 240 M-wide pair tile in multicast groups (pairs_m pairs share B: 1024 x 240 per
+    group; pairs_n pairs share sA + metadata rows: 512 x 480): vs the oracle on every output, and
+    bit-identical to the plain M-wide tile, also with few groups looping over many tiles"""
+    M, N, K = shape
+    vals, meta, _ = _dense_24(M, K, M + 7 * N + K)
+    B = tcxgen.normal_matrix((N, K), "f16", M + N, tcxgen.STREAM_B, DEV)
+    C = tcxgen.normal_matrix((M, N), "f32", M + N, tcxgen.STREAM_C, DEV)
+    hw = tcx.sp24_pack_meta(meta, M, K)
+    Dm = tcx.gemm_sp24(vals, hw, B, C, pairs=pairs, tile_m=512)
+    Dw = tcx.gemm_sp24(vals, hw, B, C, tile_m=512)
+    Dp = tcx.gemm_sp24(vals, hw, B, C, pairs=pairs, tile_m=512, max_ctas=8)
+    torch.cuda.synchronize()
+    assert torch.equal(Dm.view(torch.int32), Dw.view(torch.int32))
+    assert torch.equal(Dm.view(torch.int32), Dp.view(torch.int32))
+    ii, jj = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+    ref, absv = O.gemm_samples(O.F16, O.sp24_expand(host_bits(vals), host_bits(meta), K), host_bits(B),
+                               host_bits(C), ii.ravel(), jj.ravel())
+    fp_bound_check(host_bits(Dm).ravel(), ref, absv, K, f"sp24 mwide mc {shape} {pairs}")
+
+
 def test_sparse_multicast_bad_options_rejected():
     M, N, K = 256, 240, 128
     vals, meta, _ = _dense_24(M, K, 3)
     B = tcxgen.normal_matrix((N, K), "f16", 3, tcxgen.STREAM_B, DEV)
     hw = tcx.sp24_pack_meta(meta, M, K)
     for kw in (dict(pairs=(3, 1)), dict(pairs=(2, 1), cta_group=1), dict(pairs=(2, 1), tile_m=512)):
-        with pytest.raises(tcx.TcxError):
+        with pytest.raises(tcx.TcxError):      # (M = 256: the M-wide tile needs M % 512 == 0)
             tcx.gemm_sp24(vals, hw, B, None, **kw)
 
 

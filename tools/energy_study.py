@@ -71,21 +71,39 @@ def variant(name):
         kw = {}
         if "t256" in name:
             kw["tile_m"] = 256
-        if "pm2" in name:
+        if "pm2" in name and "mw" not in name:
             kw["tile_m"] = 256
             kw["pairs"] = (2, 1)
+        for tag, pr in (("mwpm2", (2, 1)), ("mwpn2", (1, 2)), ("mw22", (2, 2))):   # M-wide tile in multicast groups
+            if tag in name:
+                kw["tile_m"] = 512
+                kw["pairs"] = pr
+        for tag, pr in (("t256pn2", (1, 2)), ("t256p22", (2, 2))):                 # 256-row tile in groups
+            if tag in name:
+                kw["tile_m"] = 256
+                kw["pairs"] = pr
         # debug library (TCX_LIB_PATH=libtcx_debug.so) decomposition knobs: _nomma, _noload, _noepi
         kn = (2 if "_nomma" in name else 0) | (4 if "_noload" in name else 0) | (8 if "_noepi" in name else 0)
         if kn:
             kw["_knobs"] = kn
+        import re
+        mg = re.search(r"_g(m?)(\d+)", name)            # raster: _g16 = group_m 16, _gm8 = group_m -8
+        if mg:
+            kw["group_m"] = -int(mg.group(2)) if mg.group(1) else int(mg.group(2))
         return (lambda: tcx.gemm_sp24(w.vals, w.meta_hw, w.B, C, w.D, **kw)), w.flops
     if name.startswith("c3") or name.startswith("c4"):
         w = work(name[:2])
-        C = None if name.endswith("noC") else w.C
+        C = None if "noC" in name else w.C
         if name == "c3_cublas":
             out = torch.empty(8192, 8192, dtype=torch.bfloat16, device="cuda")
             return (lambda: torch.matmul(w.A, w.B.t(), out=out)), w.flops
         kw = {"tile_n": 512} if "w512" in name else {}
+        for tag, pr in (("_p12", (1, 2)), ("_p21", (2, 1)), ("_p22", (2, 2))):      # multicast clusters
+            if tag in name:
+                kw["pairs"] = pr
+        kn = (2 if "_nomma" in name else 0) | (4 if "_noload" in name else 0) | (8 if "_noepi" in name else 0)
+        if kn:                                    # debug library decomposition knobs
+            kw["_fault"] = kn
         return (lambda: tcx.gemm(w.A, w.B, C, w.D, **kw)), w.flops
     if name.startswith("probe"):
         # probe_{sp,bf16}[_rot|_areuse]: pure MMA streams on every SM (smem-resident operands); _rot reads
