@@ -128,16 +128,30 @@ def main():
             row["stream"] = st
             emit(row)
         elif cg == 2:
-            # power ceiling: pure MMA on every SM for ~2 s
-            r = run(sp, ab, cg, m, n, mode="stream", ilp=16, iters=512, repeats=1, n_acc=1, num_sms=148)
+            # power ceiling: pure MMA on every SM for ~2 s, operands N(0,1) (int8: uniform) in a 4-stage
+            # smem ring read at every k-offset (STREAM_ROT), as a GEMM mainloop reads them
+            import tcxgen
+            es = ES[ab]
+            fmt = {F16: "f16", BF16: "bf16", TF32: "tf32"}.get(ab)
+            ka, kb = 32 // es, (64 if sp else 32) // es
+            if fmt:
+                a_op = tcxgen.normal_matrix((m, ka), fmt, 1, 1, "cuda", redraw_zero=sp)
+                b_op = tcxgen.normal_matrix((n, kb), fmt, 1, 2, "cuda")
+            else:
+                a_op = tcxgen.int8_matrix((m, ka), 1, 1, "cuda")
+                b_op = tcxgen.int8_matrix((n, kb), 1, 2, "cuda")
+            prun = (lambda sp_, ab_, cg_, m_, n_, **kw:
+                   tcx.probe("tc05_sp" if sp_ else "tc05", ab_, S32 if ab_ == S8 else F32, m_, n_, (64 if sp_ else 32) // ES[ab_],
+                             cta_group=cg_, a_op=a_op, b_op=b_op, **{**kw, "mode": "stream_rot"}))
+            r = prun(sp, ab, cg, m, n, mode="stream", ilp=16, iters=512, repeats=1, n_acc=1, num_sms=148)
             per_call_s = r["ns_per_iter"] * 512 * 1e-9
             iters = int(min(2_000_000, max(512, 0.5 / max(per_call_s / 512, 1e-9))))
             with Sampler() as smp:
                 t0 = time.time()
                 rs = []
                 while time.time() - t0 < 2.0:
-                    rs.append(run(sp, ab, cg, m, n, mode="stream", ilp=16, iters=iters, repeats=1, n_acc=1,
-                                  num_sms=148))
+                    rs.append(prun(sp, ab, cg, m, n, mode="stream", ilp=16, iters=iters, repeats=1, n_acc=1,
+                                   num_sms=148))
             fma = sorted(x["fma_per_clk_per_sm"] for x in rs)[len(rs) // 2]
             mhz = sorted(x["sm_mhz"] for x in rs)[len(rs) // 2]
             emit({"power_ceiling": lab, "fma_clk_sm": round(fma, 1), "probe_mhz": round(mhz),
