@@ -465,6 +465,70 @@ def library_anchor(work, steps):
         return None
 
 
+def same_work_anchor(work, steps):
+    """C3 context: cuBLAS doing exactly this config's work — BF16 inputs, the FP32 C read and FP32 D
+    written (torch.addmm(C, A, B^T, out_dtype=float32)) — best of n; torch.matmul's BF16-out line
+    (the MEASURED_PEAKS method) skips the C read and writes half the D bytes."""
+    Bt = work.B.t()
+    out = torch.empty_like(work.D)
+    try:
+        fn = lambda: torch.addmm(work.C, work.A, Bt, out_dtype=torch.float32, out=out)
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(max(3, steps)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return round(work.flops / (best * 1e-3) / 1e12, 1), fn
+    except Exception as e:
+        log("same-work anchor unavailable:", e)
+        return None, None
+
+
+def cusparselt_anchor(work, steps=5):
+    """C5 context: cuSPARSELt (torch._cslt_sparse_mm) on the same 2:4 operand; FP16 output and no C
+    (its FP32 output is refused for FP16 inputs), i.e. less work than the config — best of n."""
+    import tcxgen as g
+    if not (getattr(torch.backends, "cusparselt", None) and torch.backends.cusparselt.is_available()):
+        return None
+    try:
+        M, N, K = work.shape
+        vals = work.vals
+        pairs = g.sp24_pairs(M, K, 0, g.STREAM_POS, work.dev).long()
+        P = torch.tensor(g.PAIRS, device=work.dev)[pairs]
+        cols = (torch.arange(K // 4, device=work.dev) * 4).view(1, -1)
+        dense = torch.zeros(M, K, dtype=vals.dtype, device=work.dev)
+        dense.scatter_(1, cols + P[..., 0], vals[:, 0::2])
+        dense.scatter_(1, cols + P[..., 1], vals[:, 1::2])
+        del pairs, P
+        comp = torch._cslt_compress(dense)
+        del dense
+        Bd = work.B.t()
+        fn = lambda: torch._cslt_sparse_mm(comp, Bd)
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del comp
+        torch.cuda.empty_cache()
+        return round(work.flops / (best * 1e-3) / 1e12, 1)
+    except Exception as e:
+        log("cuSPARSELt anchor unavailable:", e)
+        return None
+
+
 def tiles_steady_state(tcx, dev, count=524288, reps=10):
     """C1's kernel at steady state: one launch over 524,288 m16n8k16 FP16 tiles (940 MB > L2),
     CUDA events over `reps` launches; the C1 line itself is a 7 MB launch bound by launch latency."""
@@ -498,9 +562,10 @@ def roofline(work, ms, pk, clocks=None, anchor=None):
         ach = work.flops / (ms * 1e-3) / 1e12
         peak = pk["bf16"] * KIND_RATIO[work.kind]
         unit = "TFLOP/s"
-        if anchor and anchor > peak:
-            # the same-run library kernel of this dtype beat the bf16 peak x nominal ratio: it is the
-            # higher measured rate of this dtype on this box, so it is the denominator
+        if anchor and anchor > peak and KIND_RATIO[work.kind] != 1.0:
+            # a derived denominator (bf16 peak x nominal ratio) that the same-run library kernel of
+            # this dtype beat: the higher measured rate of the dtype on this box is the denominator
+            # (bf16 keeps MEASURED_PEAKS' own number, as the contract names it)
             peak, src = anchor, "same-run library anchor (best of n, this dtype and shape)"
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -860,17 +925,25 @@ def main():
                        else "64 rotating batch copies (470 MB) > L2"},
             "roofline": None, "clocks": clocks, "gpu_launches": launches,
             "e2e": e2e}
-    anchor = None
+    anchor = same_work = same_work_fn = None
     if rank == 0 and world == 1 and not args.no_extras and args.config in ("c3", "c3tf32", "c4"):
         anchor = library_anchor(work, args.steps)
+        if args.config == "c3":
+            same_work, same_work_fn = same_work_anchor(work, args.steps)
     line["roofline"] = roofline(work, ms, pk, clocks, anchor)
+    if same_work:
+        line["roofline"]["denominators"]["same_run_library_same_work"] = {
+            "peak": same_work, "frac": round(line["roofline"]["achieved"] / same_work, 4),
+            "what": "cuBLAS torch.addmm(C, A, B^T, out_dtype=float32): the same BF16 in / FP32 C in / FP32 D out"}
     if dist_on:
         line["multi_gpu"] = multi_gpu_extras(work, args, world, rank, dev, pk)
     if rank == 0 and world == 1 and not args.no_extras and args.config == "c3":
         line["context"] = {"tcx_best_of_10_steps": best_of(work),
                            "torch_matmul_bf16_tflops_same_run": anchor,
-                           "note": "cuBLAS via torch.matmul(A, B^T) on the same bf16 A, B, bf16 output (no C): "
-                                   "context only, not part of the step"}
+                           "torch_addmm_fp32_out_same_work_tflops": same_work,
+                           "note": "cuBLAS via torch.matmul(A, B^T) on the same bf16 A, B, bf16 output (no C), and via "
+                                   "torch.addmm(C, A, B^T, out_dtype=float32) doing this step's exact work: context only, "
+                                   "not part of the step"}
         also = {}
         # lightest first: the launch-bound C1 is clock-sensitive and the power-capped 2:4 runs leave
         # the board hot (C1 measured after C5 ran at ~850 MHz)
@@ -891,6 +964,9 @@ def main():
                                "clocks": ck2}
                 if extra == "c1":
                     also[extra]["steady_state"] = tiles_steady_state(w2.tcx, dev)
+                if extra == "c5":
+                    also[extra]["context"] = {"cusparselt_f16_out_no_c_tflops": cusparselt_anchor(w2),
+                                              "note": "cuSPARSELt on the same 2:4 operand, FP16 D, no C (less work): context"}
                 del w2
                 torch.cuda.empty_cache()
                 if not args.no_cpu_baseline:       # the oracle on the host cores, a bounded sample of this config
@@ -909,7 +985,10 @@ def main():
                                  "torch_matmul_bf16": sustained(work, args.sustained_s, sampler,
                                                                 fn=lambda: torch.matmul(work.A, Bt)),
                                  "note": "median of 50-step chunks over the run; MEASURED_PEAKS bf16_tflops_sustained "
-                                         "is the same method on torch.matmul"}
+                                         "is the same method on torch.matmul (BF16 out, no C)"}
+            if same_work_fn is not None:
+                line["sustained"]["torch_addmm_fp32_out_same_work"] = sustained(work, args.sustained_s, sampler,
+                                                                                fn=same_work_fn)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = oracle_sample(args.config, seconds=10.0)
         line["cpu_baseline"] = {k: (round(cb[k], 6) if isinstance(cb[k], float) else cb[k])
