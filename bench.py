@@ -424,11 +424,6 @@ def best_of(work, n=10):
     return round(work.metric_value(best * 1e-3), 2)
 
 
-def torch_matmul_anchor(work, steps):
-    """same-run cuBLAS context for C3: torch.matmul on the bench's own bf16 A, B."""
-    return library_anchor(work, steps)
-
-
 def library_anchor(work, steps):
     """the same-run library rate for this config's dtype and shape (cuBLAS through torch, no C):
     bf16 torch.matmul, TF32 torch.matmul with allow_tf32 on the same TF32-representable FP32

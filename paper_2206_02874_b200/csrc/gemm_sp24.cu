@@ -436,6 +436,10 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           // accumulator part read: MW -> M-half ch / HCH of the single buffer; else buffer `acc`
           tc05_fence_before();
           __syncwarp();
+#if TCX_WATCHDOG
+          // debug knob 16 (drain-cost experiment): hold the accumulator ~4 us longer before releasing it
+          if ((knobs & 16) && lane == 0) { const uint64_t t0 = globaltimer_ns(); while (globaltimer_ns() - t0 < 4000) {} }
+#endif
           if (lane == 0) mbar_arrive_cluster(tmem_empty_cluster + (MW ? ch / HCH : acc) * 8);
         }
         if (has_c) {

@@ -176,7 +176,6 @@ struct Tc05ProbeArgs {
   int* smid_out;
   uint32_t* acc_out;
   int* claim;        // the first active issuer to finish writes acc_out (zeroed per launch)
-  int* arrive;       // issuers = 2: CTAs resident so far (zeroed per launch)
   long long* g0;     // per issuer: %globaltimer at the start / end of the timed region
   long long* g1;
 };
@@ -408,6 +407,13 @@ tcx_status launch_probe_tc05(int grid_ctas, int issuers, const Tc05ProbeArgs& a)
   return TCX_OK;
 }
 
+// device scratch freed on every exit path (the probe returns early on errors)
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { if (p) cudaFree(p); }
+  cudaError_t alloc(size_t n) { return cudaMalloc(&p, n); }
+};
+
 double median(std::vector<double> v) {
   std::sort(v.begin(), v.end());
   if (v.empty()) return 0;
@@ -530,12 +536,14 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
   const int reps = cfg->repeats > 0 ? cfg->repeats : 5;
   const int nsm = cfg->num_sms > 0 ? std::min(cfg->num_sms, dev.sm_count) : 1;
   const int ilp = cfg->ilp > 0 ? cfg->ilp : 1;
-  long long *d_cyc = nullptr, *d_ns = nullptr;
-  uint32_t* d_sink = nullptr;
   const int nslots = 148 * 32;
-  TCX_CUDA_TRY(cudaMalloc(&d_cyc, nslots * sizeof(long long)));
-  TCX_CUDA_TRY(cudaMalloc(&d_ns, nslots * sizeof(long long)));
-  TCX_CUDA_TRY(cudaMalloc(&d_sink, 16));
+  DevBuf b_cyc, b_ns, b_sink;
+  TCX_CUDA_TRY(b_cyc.alloc(nslots * sizeof(long long)));
+  TCX_CUDA_TRY(b_ns.alloc(nslots * sizeof(long long)));
+  TCX_CUDA_TRY(b_sink.alloc(16));
+  long long* d_cyc = (long long*)b_cyc.p;
+  long long* d_ns = (long long*)b_ns.p;
+  uint32_t* d_sink = (uint32_t*)b_sink.p;
   std::vector<double> per_iter, per_ns;
   tcx_status st = TCX_OK;
   double issuers_per_sm = 1, mnk = 0;
@@ -639,20 +647,20 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
     // be chosen, and gating by %smid lets the scheduler refill vacated SMs)
     const int grid = issuers == 1 ? std::max(1, nsm / cg) * cg : dev.sm_count * 2;
     const int nclusters = grid / cg;
-    int* d_smid = nullptr;
-    TCX_CUDA_TRY(cudaMalloc(&d_smid, (grid + 2) * sizeof(int)));
-    long long* d_t = nullptr;              // cycles, ns, g0, g1 per issuer
-    TCX_CUDA_TRY(cudaMalloc(&d_t, 4 * nclusters * sizeof(long long)));
+    DevBuf b_smid, b_t;
+    TCX_CUDA_TRY(b_smid.alloc((grid + 1) * sizeof(int)));
+    TCX_CUDA_TRY(b_t.alloc(4 * nclusters * sizeof(long long)));   // cycles, ns, g0, g1 per issuer
+    int* d_smid = (int*)b_smid.p;
+    long long* d_t = (long long*)b_t.p;
     Tc05ProbeArgs pa{mode, iters, ilp, n_acc, n, alloc_cols, 1 << 30, 32, kbytes, n / cg, idesc,
                      (const uint8_t*)cfg->a_op, (const uint8_t*)cfg->b_op, d_t, d_t + nclusters,
-                     d_smid, (uint32_t*)cfg->acc_out, d_smid + grid, d_smid + grid + 1, d_t + 2 * nclusters,
-                     d_t + 3 * nclusters};
+                     d_smid, (uint32_t*)cfg->acc_out, d_smid + grid, d_t + 2 * nclusters, d_t + 3 * nclusters};
     std::vector<int> smid(grid);
     std::vector<double> rate;               // FMA per clk per SM over the union of the issuers' timed regions
     int used = 0, mx = 0;
     for (int rep = 0; rep < reps && st == TCX_OK; ++rep) {
       TCX_CUDA_TRY(cudaMemset(pa.cycles, 0xff, nclusters * sizeof(long long)));
-      TCX_CUDA_TRY(cudaMemset(pa.claim, 0, 2 * sizeof(int)));
+      TCX_CUDA_TRY(cudaMemset(pa.claim, 0, sizeof(int)));
 #define T(CGV, KV, SPV) st = launch_probe_tc05<CGV, KV, SPV>(grid, issuers, pa)
       if (cg == 1) {
         if (kind == KIND_F16) { if (sp) T(1, KIND_F16, true); else T(1, KIND_F16, false); }
@@ -700,8 +708,6 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
       out->warmup_iters = TC05_WARMUP;
       out->n_acc = n_acc;
     }
-    cudaFree(d_smid);
-    cudaFree(d_t);
     if (st == TCX_OK && !per_iter.empty()) {
       const double med = median(per_iter);
       out->cycles_per_iter_min = *std::min_element(per_iter.begin(), per_iter.end());
@@ -740,9 +746,6 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
     out->sink = sink;
   }
 done:
-  cudaFree(d_cyc);
-  cudaFree(d_ns);
-  cudaFree(d_sink);
   return st;
 }
 

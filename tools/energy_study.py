@@ -83,7 +83,8 @@ def variant(name):
                 kw["tile_m"] = 256
                 kw["pairs"] = pr
         # debug library (TCX_LIB_PATH=libtcx_debug.so) decomposition knobs: _nomma, _noload, _noepi
-        kn = (2 if "_nomma" in name else 0) | (4 if "_noload" in name else 0) | (8 if "_noepi" in name else 0)
+        kn = (2 if "_nomma" in name else 0) | (4 if "_noload" in name else 0) | (8 if "_noepi" in name else 0) | \
+             (16 if "_slowdrain" in name else 0)
         if kn:
             kw["_knobs"] = kn
         import re
