@@ -51,6 +51,9 @@ def peaks():
 
 # nominal dense ratios vs bf16 (B200_PROFILING.md nominal table: tf32 1.1 vs 2.25; int8 = fp8 rate 4.5;
 # 2:4 sparse doubles the dense rate): peak for kind = measured bf16 peak x ratio
+CFG_SHAPES = {"c3": (8192, 8192, 8192), "c3tf32": (8192, 8192, 8192), "c3f16acc": (8192, 8192, 8192),
+              "c4": (16384, 16384, 16384), "c4sp": (16384, 16384, 16384), "c3sptf32": (8192, 8192, 8192),
+              "c5": (65536, 16384, 16384), "c1": (4096,)}
 KIND_RATIO = {"bf16": 1.0, "f16": 1.0, "f16acc": 1.0, "tf32": 0.5, "s8": 2.0, "sp16": 2.0, "sp8": 4.0, "sptf32": 1.0}
 # SURVEY §8(d)'s two extra denominators: the datasheet dense BF16 peak (2.25 PFLOP/s) x the same
 # ratio, and the clock-normalised peak 148 SMs x 4096 dense BF16 FMA/clk/SM x ratio x 2 x the SM clock
@@ -852,9 +855,14 @@ def main():
         cb = oracle_sample(args.config, seconds=10.0)
         line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": cb["unit"], "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": {"c4": "s8", "c3tf32": "tf32", "c5": "f16"}.get(args.config, "bf16"),
+                "scaling": "strong", "vs_baseline": None,
+                "dtype": {"c3": "bf16", "c3tf32": "tf32", "c4": "s8", "c5": "f16", "c1": "f16", "c4sp": "s8",
+                          "c3sptf32": "tf32", "c3f16acc": "f16"}[args.config],
                 "data": "synthetic (seeded SplitMix64 / Box-Muller, tcxgen)",
-                "config": {"workload": cfg_names[args.config]},
+                "config": {"workload": cfg_names[args.config], "shape": list(CFG_SHAPES[args.config]),
+                           "parallelism": "single GPU" if args.gpus == 1 else f"row-shard x{args.gpus} (rank 0 times the oracle)",
+                           "l2": "inputs+outputs per step > 126 MiB L2 (no reuse across steps)" if args.config != "c1"
+                           else "64 rotating batch copies (470 MB) > L2"},
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
