@@ -230,13 +230,18 @@ tcx_status tcx_round_tf32(const float* in, float* out, int64_t n, void* stream);
  *                          j % cta_group, with .multicast::cluster to every CTA of the cluster;
  *                          k = 0 -> every CTA loads every box itself (unicast).  Throughput =
  *                          bytes delivered per clk per SM (the dense/sparse multicast groups).
+ *                          TMA kinds: mode bit 0 = a pseudo-random source buffer (else 0x01 bytes).
+ *   TCX_PROBE_DSMEM        clusters of cta_group (2..8) CTAs; per iteration every CTA bulk-copies ilp
+ *                          boxes of n bytes (pseudo-random) from its shared memory into the next
+ *                          CTA's (cp.async.bulk.shared::cluster, complete_tx on the receiver's
+ *                          mbarrier), waits for its own, cluster barrier: SM-to-SM forwarding rate.
  * Synchronous; allocates and frees its own scratch.  Shapes not implemented ->
  * TCX_ERR_UNSUPPORTED.
  * ------------------------------------------------------------------------------------- */
 typedef enum { TCX_PROBE_MMA_SYNC = 0, TCX_PROBE_MMA_SP_SYNC = 1, TCX_PROBE_TC05 = 2,
                TCX_PROBE_TC05_SP = 3, TCX_PROBE_LDMATRIX = 4, TCX_PROBE_LDSHARED = 5,
                TCX_PROBE_TMEM_LD = 6, TCX_PROBE_TMA_LOAD = 7, TCX_PROBE_TC05_CP = 8,
-               TCX_PROBE_TMA_MULTICAST = 9 } tcx_probe_kind;
+               TCX_PROBE_TMA_MULTICAST = 9, TCX_PROBE_DSMEM = 10 } tcx_probe_kind;
 typedef struct {
   int kind;          /* tcx_probe_kind */
   int ab, cd;        /* tcx_dtype */

@@ -356,7 +356,7 @@ def round_tf32(x, out=None):
 
 # ---------------------------------------------------------------------------------------- probe
 PROBE_KINDS = {"mma_sync": 0, "mma_sp_sync": 1, "tc05": 2, "tc05_sp": 3, "ldmatrix": 4, "ld_shared": 5,
-               "tmem_ld": 6, "tma_load": 7, "tc05_cp": 8, "tma_multicast": 9}
+               "tmem_ld": 6, "tma_load": 7, "tc05_cp": 8, "tma_multicast": 9, "dsmem": 10}
 TC05_MODES = {"sync": 0, "stream": 1, "commit": 2, "stream_rot": 3, "stream_areuse": 4}
 
 

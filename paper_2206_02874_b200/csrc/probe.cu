@@ -721,7 +721,7 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
     goto done;
   } else if (cfg->kind == TCX_PROBE_LDMATRIX || cfg->kind == TCX_PROBE_LDSHARED || cfg->kind == TCX_PROBE_TMEM_LD ||
              cfg->kind == TCX_PROBE_TMA_LOAD || cfg->kind == TCX_PROBE_TC05_CP ||
-             cfg->kind == TCX_PROBE_TMA_MULTICAST) {
+             cfg->kind == TCX_PROBE_TMA_MULTICAST || cfg->kind == TCX_PROBE_DSMEM) {
     st = run_probe_mem(dev, cfg, out);
     goto done;
   } else {

@@ -251,6 +251,62 @@ __global__ void __launch_bounds__(32, 1) probe_tma_mc_kernel(const __grid_consta
   cluster_sync();                                   // no CTA leaves while peers still write into it
 }
 
+// ---------------------------------------------------------------- distributed shared memory
+// SM-to-SM operand forwarding inside a cluster: every CTA bulk-copies ILP boxes of its own shared
+// memory into the next CTA's (cp.async.bulk.shared::cluster.shared::cta, complete_tx on the
+// destination's mbarrier), waits for its predecessor's boxes, then the cluster syncs (flow
+// control).  The payload is pseudo-random (toggling like real operands).  Throughput = bytes
+// received per clk per SM — the alternative to re-reading a shared operand from L2.
+__global__ void __launch_bounds__(32, 1) probe_dsmem_kernel(int iters, int ilp, uint32_t box_bytes, long long* cycles,
+                                                            long long* ns) {
+  extern __shared__ uint8_t dyn[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)dyn + 127) & ~(uintptr_t)127);
+  uint8_t* src = base;
+  uint8_t* dst = base + (size_t)ilp * box_bytes;
+  __shared__ uint64_t bar;
+  const uint32_t cs = cluster_nctarank(), r = cluster_ctarank();
+  for (uint32_t i = threadIdx.x; i < ilp * box_bytes / 4; i += 32) {
+    uint32_t x = i * 2654435761u + blockIdx.x * 40503u;
+    x ^= x >> 15; x *= 0x2c1b3c6dU; x ^= x >> 12;
+    ((uint32_t*)src)[i] = x;
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  cluster_sync();
+  if (threadIdx.x == 0) {
+    const uint32_t peer = (r + 1) % cs;
+    const uint32_t dst_peer = mapa(smem_u32(dst), peer), bar_peer = mapa(smem_u32(&bar), peer);
+    uint32_t phase = 0;
+    long long t0 = 0; uint64_t g0 = 0;
+    for (int it = -4; it < iters; ++it) {
+      if (it == 0) { t0 = clock64(); g0 = gtimer(); }
+      mbar_arrive_expect_tx(&bar, (uint32_t)ilp * box_bytes);
+      for (int s2 = 0; s2 < ilp; ++s2)
+        asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     :: "r"(dst_peer + s2 * box_bytes), "r"(smem_u32(src + s2 * box_bytes)), "r"(box_bytes), "r"(bar_peer)
+                     : "memory");
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+    }
+    const long long t1 = clock64();
+    const uint64_t g1 = gtimer();
+    cycles[blockIdx.x * 32] = t1 - t0;
+    ns[blockIdx.x * 32] = (long long)(g1 - g0);
+  } else {
+    for (int it = -4; it < iters; ++it) asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+  }
+  cluster_sync();
+}
+
+__global__ void fill_random_kernel(uint32_t* p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t x = (uint32_t)i * 2654435761u + 0x9E3779B9u;
+    x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+    p[i] = x;
+  }
+}
+
 // ---------------------------------------------------------------- tcgen05.cp (smem -> TMEM)
 // the sparse path's metadata staging: ILP tcgen05.cp.cta_group::1.128x128b (2 KiB each) into
 // distinct TMEM columns, then tcgen05.commit -> mbarrier wait.
@@ -387,7 +443,8 @@ tcx_status run_probe_mem(const DevInfo& dev, const tcx_probe_config* cfg, tcx_pr
       }
       if (!tma_src) {
         if (cudaMalloc(&tma_src, 4096u * 4096u) != cudaSuccess) { st = set_error(TCX_ERR_CUDA, "probe: cudaMalloc"); break; }
-        cudaMemset(tma_src, 1, 4096u * 4096u);
+        if (cfg->mode & 1) fill_random_kernel<<<592, 256>>>((uint32_t*)tma_src, 4096u * 4096u / 4);
+        else cudaMemset(tma_src, 1, 4096u * 4096u);
       }
       CUtensorMap tm;
       st = make_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, tma_src, 4096, 4096, 4096, (uint32_t)inner, (uint32_t)rows,
@@ -409,7 +466,8 @@ tcx_status run_probe_mem(const DevInfo& dev, const tcx_probe_config* cfg, tcx_pr
       }
       if (!tma_src) {
         if (cudaMalloc(&tma_src, 4096u * 4096u) != cudaSuccess) { st = set_error(TCX_ERR_CUDA, "probe: cudaMalloc"); break; }
-        cudaMemset(tma_src, 1, 4096u * 4096u);
+        if (cfg->mode & 1) fill_random_kernel<<<592, 256>>>((uint32_t*)tma_src, 4096u * 4096u / 4);
+        else cudaMemset(tma_src, 1, 4096u * 4096u);
       }
       CUtensorMap tm;
       st = make_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, tma_src, 4096, 4096, 4096, (uint32_t)inner, (uint32_t)rows,
@@ -435,6 +493,29 @@ tcx_status run_probe_mem(const DevInfo& dev, const tcx_probe_config* cfg, tcx_pr
       le = cudaLaunchKernelEx(&lc, probe_tma_mc_kernel, tm, iters, ilp, rows, (uint32_t)(rows * inner), 4096,
                               cfg->k ? 1 : 0, d_cyc, d_ns);
       if (le != cudaSuccess) { st = set_error(TCX_ERR_CUDA, "probe multicast launch: %s", cudaGetErrorString(le)); break; }
+      warps_eff = 1;
+    } else if (cfg->kind == TCX_PROBE_DSMEM) {
+      // cluster of cta_group (2..8) CTAs, ilp boxes of n bytes (multiple of 16) forwarded per iteration
+      const int cs = cfg->cta_group >= 2 ? cfg->cta_group : 2;
+      const int box = cfg->n > 0 ? cfg->n : 16384;
+      if (cs > 8 || box % 16 || 2 * box * ilp > 200 * 1024) {
+        st = set_error(TCX_ERR_UNSUPPORTED, "tcx_probe: DSMEM cluster 2..8, n %% 16 == 0, 2*ilp*n <= 200 KiB");
+        break;
+      }
+      const int smem = 2 * box * ilp + 128;
+      cudaFuncSetAttribute(probe_dsmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaLaunchConfig_t lc = {};
+      launched = std::max(cs, (nsm / cs) * cs);
+      lc.gridDim = dim3(launched);
+      lc.blockDim = dim3(32);
+      lc.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      lc.attrs = at; lc.numAttrs = 1;
+      bytes_per_warp_iter = (double)box * ilp;
+      cudaError_t le2 = cudaLaunchKernelEx(&lc, probe_dsmem_kernel, iters, ilp, (uint32_t)box, d_cyc, d_ns);
+      if (le2 != cudaSuccess) { st = set_error(TCX_ERR_CUDA, "probe DSMEM launch: %s", cudaGetErrorString(le2)); break; }
       warps_eff = 1;
     } else if (cfg->kind == TCX_PROBE_TC05_CP) {
       bytes_per_warp_iter = 2048.0 * ilp;

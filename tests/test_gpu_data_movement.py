@@ -86,6 +86,16 @@ def test_tma_multicast_probe():
         _p("tma_multicast", m=128, n=128, ilp=6, cta_group=4, k=1)      # ilp must split over the cluster
 
 
+def test_dsmem_forwarding_probe():
+    """SM-to-SM bulk copies inside clusters of 2 and 4 CTAs complete every wait (a lost complete_tx
+    would hang) at a positive rate; how it compares with TMA from L2 is a measurement"""
+    for cs in (2, 4):
+        r = _p("dsmem", n=16384, ilp=4, cta_group=cs, num_sms=148, iters=256)
+        assert r["latency_cycles"] > 0 and r["fma_per_clk_per_sm"] > 1, (cs, r)
+    with pytest.raises(tcx.TcxError):
+        _p("dsmem", n=16384 + 8, ilp=2, cta_group=2)                  # box must be a multiple of 16 B
+
+
 def test_data_movement_sweep_report():
     rep = {"units": {"latency": "cycles per iteration (clock64)", "throughput": "bytes/clk/SM"},
            "paper_A100_context": {

@@ -134,6 +134,17 @@ def variant(name):
         iters = 20000
         return (lambda: tcx.probe("tma_load", tcx.S8, tcx.S32, 128, 128, 0, ilp=8, iters=iters, repeats=1,
                                   num_sms=148)), float(148 * (iters + 4) * 8 * 128 * 128)
+    if name == "tma_l2_rand":
+        # as tma_l2, the L2-resident source filled with pseudo-random bytes (toggles like operands)
+        iters = 20000
+        return (lambda: tcx.probe("tma_load", tcx.S8, tcx.S32, 128, 128, 0, ilp=8, iters=iters, repeats=1,
+                                  num_sms=148, mode=1)), float(148 * (iters + 4) * 8 * 128 * 128)
+    if name.startswith("dsmem"):
+        # SM-to-SM forwarding inside clusters of 2 (dsmem2) or 4 (dsmem4): 4 x 16 KiB random boxes
+        cs = int(name[5:])
+        iters = 20000
+        return (lambda: tcx.probe("dsmem", tcx.S8, tcx.S32, 0, 16384, 0, cta_group=cs, ilp=4, iters=iters, repeats=1,
+                                  num_sms=148)), float((148 // cs) * cs * (iters + 4) * 4 * 16384)
     if name == "dram_copy":
         # HBM alone: a 2 GiB random buffer copied (read + write bytes), far beyond L2
         if "dram" not in WORK:
@@ -187,7 +198,8 @@ def measure(name, seconds, nv):
             "J_per_launch": round(joules / n, 4), "W": round(joules / (t1 - t0), 1),
             "tflops": round(flops / (ms * 1e-3) / 1e12, 1) if flops else None,
             "pJ_per_flop": round(joules / n / flops * 1e12, 4) if flops else None,
-            "note": "tma_l2 / dram_copy: 'tflops' and 'pJ_per_flop' are per BYTE moved" if name in ("tma_l2", "dram_copy") else None,
+            "note": "data-movement variant: 'tflops' and 'pJ_per_flop' are per BYTE moved"
+            if name in ("tma_l2", "tma_l2_rand", "dram_copy") or name.startswith("dsmem") else None,
             "sm_mhz_median": mhz[len(mhz) // 2] if mhz else None,
             "power_cap_frac": round(sum(1 for x in s if x[1] & 4) / max(1, len(s)), 2)}
 
