@@ -488,6 +488,30 @@ def same_work_anchor(work, steps):
         return None, None
 
 
+def power_roofline(kind, seconds=2.0):
+    """The tensor cores alone at the board's power cap: tcx_probe STREAM_ROT on
+    every SM — CTA-pair MMAs of this config's kind on N(0,1) operands read from a 4-stage smem ring,
+    no operand loads, no epilogue — back to back for ~`seconds`; returns the median call's
+    dense-equivalent TFLOP/s.  No GEMM can exceed it at the cap: it is the power roofline."""
+    import tcxgen as g
+    import paper_2206_02874_b200 as tcx
+    sp = kind == "sp16"
+    ab, fmt, n, k = (tcx.F16, "f16", 240, 32) if sp else (tcx.BF16, "bf16", 256, 16)
+    a = g.normal_matrix((256, 16), fmt, 1, 1, "cuda", redraw_zero=sp)
+    b = g.normal_matrix((n, k), fmt, 1, 2, "cuda")
+    call = lambda it: tcx.probe("tc05_sp" if sp else "tc05", ab, tcx.F32, 256, n, k, cta_group=2, ilp=16, iters=it,
+                                repeats=1, num_sms=148, n_acc=1, mode="stream_rot", a_op=a, b_op=b)
+    r = call(512)
+    iters = int(min(2_000_000, max(512, 0.25 / max(r["ns_per_iter"] * 1e-9, 1e-9))))   # ~0.25 s per call
+    vals = []
+    t0 = time.time()
+    while time.time() - t0 < seconds:
+        r = call(iters)
+        vals.append(2.0 * r["fma_per_clk_per_sm"] * 148 * r["sm_mhz"] * 1e6 / 1e12)
+    vals.sort()
+    return round(vals[len(vals) // 2], 1)
+
+
 def cusparselt_anchor(work, steps=5):
     """C5 context: cuSPARSELt (torch._cslt_sparse_mm) on the same 2:4 operand; FP16 output and no C
     (its FP32 output is refused for FP16 inputs), i.e. less work than the config — best of n."""
@@ -970,6 +994,13 @@ def main():
                 if extra == "c5":
                     also[extra]["context"] = {"cusparselt_f16_out_no_c_tflops": cusparselt_anchor(w2),
                                               "note": "cuSPARSELt on the same 2:4 operand, FP16 D, no C (less work): context"}
+                    try:
+                        pr = power_roofline("sp16")
+                        also[extra]["roofline"]["denominators"]["power_capped_mma_only"] = {
+                            "peak": pr, "frac": round(also[extra]["roofline"]["achieved"] / pr, 4),
+                            "what": "tcx_probe: 2:4 f16 CTA-pair MMAs alone on all SMs, N(0,1) operands, at the cap"}
+                    except Exception as e:  # report, never hide
+                        also[extra]["context"]["power_roofline_error"] = f"{type(e).__name__}: {e}"
                 del w2
                 torch.cuda.empty_cache()
                 if not args.no_cpu_baseline:       # the oracle on the host cores, a bounded sample of this config
@@ -980,6 +1011,14 @@ def main():
             except Exception as e:  # report, never hide
                 also[extra] = {"error": f"{type(e).__name__}: {e}"}
         line["also"] = also
+        # after the extras (it leaves the board at its power cap): the headline's power roofline
+        try:
+            pr = power_roofline("bf16")
+            line["roofline"]["denominators"]["power_capped_mma_only"] = {
+                "peak": pr, "frac": round(line["roofline"]["achieved"] / pr, 4),
+                "what": "tcx_probe: bf16 CTA-pair MMAs alone on all SMs, N(0,1) operands, at the 1000 W cap (~2 s)"}
+        except Exception as e:  # report, never hide
+            line["roofline"]["denominators"]["power_capped_mma_only"] = {"error": f"{type(e).__name__}: {e}"}
         if args.sustained_s > 0:
             # 4 s back to back at the power cap, ours and the cuBLAS anchor, beside the burst value
             # (after the extras: it leaves the board hot, and the launch-bound C1 is clock-sensitive)

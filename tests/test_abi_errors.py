@@ -102,3 +102,6 @@ def test_tiles_and_chain_argument_errors():
     assert L.tcx_mma_chain(F16, 0, 4, P, P, P, None) == OK
     assert L.tcx_round_tf32(None, None, -1, None) == INVALID
     assert L.tcx_round_tf32(None, None, 0, None) == OK
+    assert L.tcx_sm_clock_stamp(None, 4, None) == INVALID
+    assert L.tcx_sm_clock_stamp(P, 0, None) == INVALID
+    assert L.tcx_sm_clock_stamp(P + 4, 4, None) == MISALIGNED

@@ -80,3 +80,22 @@ def test_dependent_calls_stay_ordered():
     ref_t = 6 * torch.einsum("tik,tjk->tij", At.double(), Bt.double())
     torch.cuda.synchronize()
     assert torch.equal(Dt.double(), ref_t)
+
+
+def test_sm_clock_stamp_measures_the_sm_clock():
+    """tcx_sm_clock_stamp (the bench's in-run clock): two stamps around a busy GEMM give every SM's
+    average clock; it must be a sane B200 SM clock and agree with the probe's clock64/globaltimer
+    ratio to within a generous margin (power management moves the clock between runs)."""
+    import paper_2206_02874_b200 as tcx
+    s0 = torch.zeros(2 * 256, dtype=torch.int64, device="cuda")
+    s1 = torch.zeros_like(s0)
+    A = torch.randn(4096, 4096, device="cuda").to(torch.bfloat16)
+    tcx.sm_clock_stamp(s0)
+    for _ in range(10):
+        tcx.gemm(A, A)
+    tcx.sm_clock_stamp(s1)
+    torch.cuda.synchronize()
+    mhz = tcx.sm_mhz_between(s0, s1)
+    assert mhz is not None and 300 < mhz < 2200, mhz
+    stamped = int(((s0.view(-1, 2)[:, 1] > 0) & (s1.view(-1, 2)[:, 1] > 0)).sum())
+    assert stamped >= 140, stamped                     # (nearly) every SM ran a stamp CTA
