@@ -119,7 +119,9 @@ typedef struct {
                    /* hardware forms the cluster, A (sA) is TMA-multicast across the pairs_n pairs  */
                    /* of a row and B across the pairs_m pairs of a column; elsewhere the pairs load */
                    /* their own operands.  1 or 2 each; 0 = default 1.  Results are bit-identical  */
-                   /* to the default.                                                               */
+                   /* to the default.  0 = library choice: for tcx_gemm with the CTA pair and at   */
+                   /* least two waves of 256 x 256 tiles over >= 2 tile columns, 1 x 2 (A shared);  */
+                   /* 1 x 1 otherwise; pass 1 / 1 to force plain pairs.                            */
   int reserved[2]; /* 0.  reserved[0] = 1 in the debug library (libtcx_debug.so) only: the dense
                       producer drops one TMA load (fault injection for the watchdog tests);
                       the product library ignores it */

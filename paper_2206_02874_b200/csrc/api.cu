@@ -264,6 +264,7 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
                        "32-bit accumulator");
     g.pairs_m = pm;
     g.pairs_n = pn;
+    g.pairs_auto = opts->pairs_m == 0 && opts->pairs_n == 0 && opts->cta_group != 1 && g.tile_n != 512;
 #if TCX_WATCHDOG
     g.fault = opts->reserved[0];   // fault injection exists only in the debug library
 #endif

@@ -58,6 +58,7 @@ struct GemmArgs {
   int tile_n;     // dense: 256 / 512 / 0 = auto
   int pairs_m = 1;  // dense, CTA pair: multicast cluster shape in pairs
   int pairs_n = 1;
+  bool pairs_auto = true;   // dense: the caller left pairs_m / pairs_n at 0 (library choice)
   int fault = 0;    // debug builds only (TCX_WATCHDOG): 1 = the dense producer drops one TMA load
   uint64_t* trace = nullptr;   // debug builds only: tile timeline (tcx_debug_trace)
   int64_t trace_cap = 0;
