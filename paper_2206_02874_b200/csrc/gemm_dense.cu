@@ -50,16 +50,23 @@ struct Cfg {
   static constexpr int A_BYTES = BM * KBYTES;                    // 16 KiB
   static constexpr int B_BYTES = NH * HALF_BYTES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = NH == 2 ? 3 : (CG == 1 ? 4 : 6);
+#ifndef TCX_DENSE_STAGES          // experiment knobs (tools/build_variant.py); defaults are the product's
+#define TCX_DENSE_STAGES 6
+#endif
+#ifndef TCX_DENSE_NBE
+#define TCX_DENSE_NBE 2
+#endif
+  static constexpr int STAGES = NH == 2 ? 3 : (CG == 1 ? 4 : TCX_DENSE_STAGES);
   // epilogue staging buffers per warp (4 KiB each) and how far ahead C is loaded: the wide tile's
   // single accumulator puts the epilogue on the critical path, so it trades a ring stage for depth
-  static constexpr int NBE = NH == 2 ? 4 : 2;
+  static constexpr int NBE = NH == 2 ? 4 : (CG == 1 ? 2 : TCX_DENSE_NBE);
   static constexpr int C_AHEAD = NBE == 2 ? 2 : NBE - 1;
   static constexpr int NBUF = 2 / NH;                            // TMEM accumulator buffers
   static constexpr int SMEM_DATA = STAGES * STAGE_BYTES;
   static constexpr int STG_BYTES = EPI_WARPS * NBE * 4096;       // epilogue: NBE x 4 KiB per warp
   static constexpr int SMEM_TOTAL = SMEM_DATA + STG_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
   static_assert(NH == 1 || CG == 2, "wide tiles need the CTA pair");
+  static_assert(SMEM_TOTAL <= 232448, "smem budget");
 };
 
 // FP16 inputs with an FP16 accumulator (idesc c_format F16; the f16.f16.f16.f16 MMA of PAPER.md:428-429

@@ -35,7 +35,7 @@ def main():
         for v in (variants if r % 2 == 0 else variants[::-1]):
             kw = parse(v)
             if sparse:
-                w.step = lambda: w.tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, **kw)
+                w.step = lambda: w.tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, tf32=cfg == "c3sptf32", **kw)
             else:
                 w.step = lambda: w.tcx.gemm(w.A, w.B, w.C, w.D, tf32=getattr(w, "tf32", False),
                                             f16_acc=cfg == "c3f16acc", **kw)
