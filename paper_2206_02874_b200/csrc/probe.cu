@@ -167,7 +167,7 @@ tcx_status launch_probe_mma(int ilp, int grid, int warps, int iters, long long* 
 // issuers = 2 launches two CTAs per SM on every SM (the smem request caps residency at two); %smid of
 // every CTA is recorded so the co-residency is checked, not assumed.
 struct Tc05ProbeArgs {
-  int mode, iters, ilp, n_acc, acc_cols, alloc_cols, num_sms, a_bytes, b_bytes, n_rows;
+  int mode, iters, ilp, n_acc, acc_cols, alloc_cols, a_bytes, b_bytes, n_rows;
   uint32_t idesc;
   const uint8_t* a_op;
   const uint8_t* b_op;
@@ -193,23 +193,12 @@ probe_tc05_kernel(const Tc05ProbeArgs p) {
   uint8_t* sb = smem + 16384;         // up to 256 rows x 128 B (SW128) per stage
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base_s;
-  __shared__ int smid_s;
   const int warp = threadIdx.x / 32;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
   if (threadIdx.x == 0) {
     int sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    smid_s = sm;
+    p.smid_out[blockIdx.x] = sm;                  // co-residency (issuers per SM) is checked, not assumed
   }
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
-  int lead_smid = smid_s;
-  if constexpr (CG == 2) {
-    uint32_t a = mapa(smem_u32(&smid_s), 0);
-    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(lead_smid) : "r"(a) : "memory");
-  }
-  const bool active = lead_smid < p.num_sms;
-  if (threadIdx.x == 0) p.smid_out[blockIdx.x] = active ? smid_s : -1;
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();   // peer's smid read before anyone exits
-  if (!active) return;
   // operands: this CTA's A rows (rank * 128 ..) and B rows (rank * n_rows ..), SW128 placement.  The
   // rotating modes read TC05_STAGES stage buffers at every k-offset of the 128-byte row (like a GEMM
   // ring): each row's operand bytes are replicated into every slot, so every MMA still computes the
@@ -652,7 +641,7 @@ tcx_status run_probe(const DevInfo& dev, const tcx_probe_config* cfg, tcx_probe_
     TCX_CUDA_TRY(b_t.alloc(4 * nclusters * sizeof(long long)));   // cycles, ns, g0, g1 per issuer
     int* d_smid = (int*)b_smid.p;
     long long* d_t = (long long*)b_t.p;
-    Tc05ProbeArgs pa{mode, iters, ilp, n_acc, n, alloc_cols, 1 << 30, 32, kbytes, n / cg, idesc,
+    Tc05ProbeArgs pa{mode, iters, ilp, n_acc, n, alloc_cols, 32, kbytes, n / cg, idesc,
                      (const uint8_t*)cfg->a_op, (const uint8_t*)cfg->b_op, d_t, d_t + nclusters,
                      d_smid, (uint32_t*)cfg->acc_out, d_smid + grid, d_t + 2 * nclusters, d_t + 3 * nclusters};
     std::vector<int> smid(grid);
