@@ -130,6 +130,14 @@ class ClockSampler:
                 "power_w_median": round(statistics.median(pw), 1) if pw else None}
 
 
+def dense_kernel_name(kind, M, N, sm_count=148):
+    """the dense kernel instance the library picks by default (gemm_dense.cu auto_pairs_1x2): 1 x 2
+    multicast groups once there are >= 2 waves of 256 x 256 pair tiles over >= 2 tile columns"""
+    m_tiles, n_tiles = (M + 255) // 256, (N + 255) // 256
+    groups = n_tiles >= 2 and m_tiles * n_tiles >= 2 * (sm_count // 2)
+    return f"gemm_dense_kernel<2,{kind},1,1,{2 if groups else 1}>" + (" (1x2 groups)" if groups else "")
+
+
 # ----------------------------------------------------------------------------------- workloads
 class Work:
     """one config on this rank: inputs resident in HBM, step() launches the hot path once."""
@@ -159,7 +167,7 @@ class Work:
             self.flops = 2.0 * (m1 - m0) * N * K
             self.alg_bytes = self.A.numel() * self.A.element_size() + self.B.numel() * self.B.element_size() + 8 * (m1 - m0) * N
             self.tf32 = fmt == "tf32"
-            self.kernel = "gemm_dense_kernel<2,%d>" % (0 if fmt == "bf16" else 1)
+            self.kernel = dense_kernel_name(0 if fmt == "bf16" else 1, m1 - m0, N)
             self.step = lambda: tcx.gemm(self.A, self.B, self.C, self.D, tf32=self.tf32)
             self.unit, self.bound = "TFLOP/s", "tensor"
         elif cfg == "c3f16acc":              # NEXT-2: FP16 inputs, FP16 accumulator, FP16 C/D at C3's shape
@@ -173,7 +181,7 @@ class Work:
             self.D = torch.empty(m1 - m0, N, dtype=torch.float16, device=dev)
             self.flops = 2.0 * (m1 - m0) * N * K
             self.alg_bytes = 2 * (self.A.numel() + self.B.numel()) + 4 * (m1 - m0) * N
-            self.kernel = "gemm_dense_kernel<2,f16acc>"
+            self.kernel = dense_kernel_name("f16acc", m1 - m0, N)
             self.step = lambda: tcx.gemm(self.A, self.B, self.C, self.D, f16_acc=True)
             self.unit, self.bound = "TFLOP/s", "tensor"
         elif cfg == "c4":
@@ -187,7 +195,7 @@ class Work:
             self.D = torch.empty(m1 - m0, N, dtype=torch.int32, device=dev)
             self.flops = 2.0 * (m1 - m0) * N * K
             self.alg_bytes = self.A.numel() + self.B.numel() + 8 * (m1 - m0) * N
-            self.kernel = "gemm_dense_kernel<2,2>"
+            self.kernel = dense_kernel_name(2, m1 - m0, N)
             self.step = lambda: tcx.gemm(self.A, self.B, self.C, self.D)
             self.unit, self.bound = "TOPS", "tensor"
         elif cfg in ("c5", "c5s"):       # c5s: an 8192-row slice of C5 (profiling only)
@@ -208,7 +216,8 @@ class Work:
             # (kept-product) rate is half of it and is reported beside it (DESIGN.md R-C13)
             self.flops = 2.0 * (m1 - m0) * N * K
             self.alg_bytes = self.vals.numel() * 2 + self.meta_hw.numel() + self.B.numel() * 2 + 8 * (m1 - m0) * N
-            self.kernel = "gemm_sp24_kernel"
+            mw = (m1 - m0) % 512 == 0 and (m1 - m0) * N * K >= 2 ** 43      # gemm_sp24.cu's M-wide default
+            self.kernel = "gemm_sp24_kernel<2,f16,M-wide 512x240>" if mw else "gemm_sp24_kernel<2,f16,256x240>"
             self.step = lambda: tcx.gemm_sp24(self.vals, self.meta_hw, self.B, self.C, self.D)
             self.unit, self.bound = "TFLOP/s", "tensor"
         elif cfg in ("c4sp", "c3sptf32"):   # NEXT-1: INT8 2:4 at C4's shape, TF32 1:2 at C3's shape
