@@ -247,8 +247,8 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           }
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&sm->full[stage], C_::STAGE_BYTES);
-            tma_load_2d(sa, &tmA, &sm->full[stage], kx, arow);
-            tma_load_2d(sb, &tmB, &sm->full[stage], kx, brow);
+            tma_load_2d<HINT_AB>(sa, &tmA, &sm->full[stage], kx, arow, l2_policy_ab());
+            tma_load_2d<HINT_AB>(sb, &tmB, &sm->full[stage], kx, brow, l2_policy_ab());
           } else {
             if (leader) mbar_arrive_expect_tx(&sm->full[stage], 2 * C_::STAGE_BYTES);
             const uint32_t bar = full0_cluster + stage * 8;
@@ -263,19 +263,19 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
             (void)fault; (void)trace; (void)trace_cap;
 #endif
             if (PN > 1 && mc) {
-              tma_load_2d_cg2_mc(sa + pn * A_ROWS * KBYTES, &tmA, bar, kx, arow + pn * A_ROWS, mask_a);
+              tma_load_2d_cg2_mc<HINT_AB>(sa + pn * A_ROWS * KBYTES, &tmA, bar, kx, arow + pn * A_ROWS, mask_a, l2_policy_ab());
             } else {
 #pragma unroll
-              for (int j = 0; j < PN; ++j) tma_load_2d_cg2(sa + j * A_ROWS * KBYTES, &tmA, bar, kx, arow + j * A_ROWS);
+              for (int j = 0; j < PN; ++j) tma_load_2d_cg2<HINT_AB>(sa + j * A_ROWS * KBYTES, &tmA, bar, kx, arow + j * A_ROWS, l2_policy_ab());
             }
             if (PM > 1 && mc) {
-              tma_load_2d_cg2_mc(sb + pm * B_ROWS * KBYTES, &tmB, bar, kx, brow + pm * B_ROWS, mask_b);
+              tma_load_2d_cg2_mc<HINT_AB>(sb + pm * B_ROWS * KBYTES, &tmB, bar, kx, brow + pm * B_ROWS, mask_b, l2_policy_ab());
             } else {
 #pragma unroll
               for (int h = 0; h < NH; ++h)
 #pragma unroll
                 for (int i = 0; i < PM; ++i)
-                  tma_load_2d_cg2(sb + h * C_::HALF_BYTES + i * B_ROWS * KBYTES, &tmB, bar, kx, brow + h * BN + i * B_ROWS);
+                  tma_load_2d_cg2<HINT_AB>(sb + h * C_::HALF_BYTES + i * B_ROWS * KBYTES, &tmB, bar, kx, brow + h * BN + i * B_ROWS, l2_policy_ab());
             }
           }
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
@@ -426,7 +426,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         if (lane == 0) {
           int x, y; coords(it, ch, x, y);
           mbar_arrive_expect_tx(&cbar[ch & 1], 2048);
-          tma_load_2d(stg + (ch & 1) * 2048, &tmC, &cbar[ch & 1], x, y);
+          tma_load_2d<HINT_C>(stg + (ch & 1) * 2048, &tmC, &cbar[ch & 1], x, y, l2_evict_first());
         }
       };
       load(0);
@@ -481,7 +481,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         __syncwarp();
         if (lane == 0) {
           int x, y; coords(it, ch, x, y);
-          tma_store_2d(&tmD, stg + b * 2048, x, y);
+          tma_store_2d<HINT_D>(&tmD, stg + b * 2048, x, y, l2_evict_first());
           bulk_commit();
         }
       }
@@ -535,7 +535,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         int x, y; coords(q, x, y);
         const int bq = (int)(q % C_::NBE);
         mbar_arrive_expect_tx(&cbar[bq], 4096);
-        tma_load_2d(stg + bq * 4096, &tmC, &cbar[bq], x, y);
+        tma_load_2d<HINT_C>(stg + bq * 4096, &tmC, &cbar[bq], x, y, l2_evict_first());
       }
     };
     // single-buffered (wide) tiles: the epilogue is on the critical path, so each tile's C is
@@ -543,7 +543,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     // — except the first tile's, prefetched while the mainloop starts: small problems are one tile)
     auto prefetch_c_tile = [&](int64_t it) {
       if ((NH == 2 || it == 0) && has_c && lane == 0 && it < my_tiles)
-        for (int ch = 0; ch < CH; ++ch) { int x, y; coords(it * CH + ch, x, y); tma_prefetch_2d(&tmC, x, y); }
+        for (int ch = 0; ch < CH; ++ch) { int x, y; coords(it * CH + ch, x, y); tma_prefetch_2d<HINT_C>(&tmC, x, y, l2_evict_first()); }
     };
     prefetch_c_tile(0);
     for (int c = 0; c < C_::C_AHEAD; ++c) load_c(c);
@@ -573,7 +573,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           mbar_arrive_expect_tx(&sm->cring[e], CH * 4096);
           for (int ch = 0; ch < CH; ++ch) {
             int x, y; coords(it * CH + ch, x, y);
-            tma_load_2d(ring_stg + ch * 4096, &tmC, &sm->cring[e], x, y);
+            tma_load_2d<HINT_C>(ring_stg + ch * 4096, &tmC, &sm->cring[e], x, y, l2_evict_first());
           }
         }
         __syncwarp();
@@ -642,7 +642,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         TCX_STAMP(it, ch, 4);
         if (lane == 0 && !k_noepi) {
           int x, y; coords(q, x, y);
-          tma_store_2d(&tmD, buf, x, y);
+          tma_store_2d<HINT_D>(&tmD, buf, x, y, l2_evict_first());
           bulk_commit();
           TCX_STAMP(it, ch, 5);
           // the buffer of chunk q + C_AHEAD was last read by the store of chunk q + C_AHEAD - NBE

@@ -238,14 +238,14 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
           const uint32_t bar = CG == 2 ? full0_cluster + stage * 8 : smem_u32(&sm->full[stage]);
           auto load = [&](void* dst, const CUtensorMap* m, int x, int y) {
-            if constexpr (CG == 1) tma_load_2d(dst, m, &sm->full[stage], x, y);
-            else tma_load_2d_cg2(dst, m, bar, x, y);
+            if constexpr (CG == 1) tma_load_2d<HINT_AB>(dst, m, &sm->full[stage], x, y, l2_policy_ab());
+            else tma_load_2d_cg2<HINT_AB>(dst, m, bar, x, y, l2_policy_ab());
           };
 #pragma unroll
           for (int h = 0; h < MH; ++h) {
             const int64_t mrow_h = mrow + h * BM * CG;
             if (PN > 1 && mc) {
-              tma_load_2d_cg2_mc(sa + h * C_::A_HALF + pn * A_ROWS * 128, &tmA, bar, ka, (int)mrow_h + pn * A_ROWS, mask_a);
+              tma_load_2d_cg2_mc<HINT_AB>(sa + h * C_::A_HALF + pn * A_ROWS * 128, &tmA, bar, ka, (int)mrow_h + pn * A_ROWS, mask_a, l2_policy_ab());
             } else {
 #pragma unroll
               for (int j = 0; j < PN; ++j) load(sa + h * C_::A_HALF + j * A_ROWS * 128, &tmA, ka, (int)mrow_h + j * A_ROWS);
@@ -253,7 +253,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             load(se + h * 2048 * C_::META_ATOMS, &tmE, 0, (int)(((mrow_h / 128) * k_blocks + kb) * 16 * C_::META_ATOMS));
           }
           if (PM > 1 && mc) {
-            tma_load_2d_cg2_mc(sb + pm * C_::B_HALF, &tmB, bar, kx + pm * C_::BOX, brow, mask_b);
+            tma_load_2d_cg2_mc<HINT_AB>(sb + pm * C_::B_HALF, &tmB, bar, kx + pm * C_::BOX, brow, mask_b, l2_policy_ab());
           } else {
             load(sb, &tmB, kx, brow);
             load(sb + C_::B_HALF, &tmB, kx + C_::BOX, brow);
@@ -402,14 +402,14 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         int x, y; coords(q, x, y);
         const int bq = (int)(q % STG_BUFS);
         mbar_arrive_expect_tx(&cbar[bq], 2048);
-        tma_load_2d(stg + bq * 2048, &tmC, &cbar[bq], x, y);
+        tma_load_2d<HINT_C>(stg + bq * 2048, &tmC, &cbar[bq], x, y, l2_evict_first());
       }
     };
     // single-buffered (wide) tiles: the epilogue is on the critical path, so each tile's C is
     // L2-prefetched a tile ahead and its chunk loads hit L2 (double-buffered tiles hide the latency)
     auto prefetch_c_tile = [&](int64_t it) {
       if (MW && has_c && lane == 0 && it < my_tiles)
-        for (int ch = 0; ch < CH; ++ch) { int x, y; coords(it * CH + ch, x, y); tma_prefetch_2d(&tmC, x, y); }
+        for (int ch = 0; ch < CH; ++ch) { int x, y; coords(it * CH + ch, x, y); tma_prefetch_2d<HINT_C>(&tmC, x, y, l2_evict_first()); }
     };
     prefetch_c_tile(0);
     load_c(0);
@@ -476,7 +476,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         __syncwarp();
         if (lane == 0 && !k_noepi) {
           int x, y; coords(q, x, y);
-          tma_store_2d(&tmD, stg + b * 2048, x, y);
+          tma_store_2d<HINT_D>(&tmD, stg + b * 2048, x, y, l2_evict_first());
           bulk_commit();
           // the buffer of chunk q + C_AHEAD was last read by the store of chunk q + C_AHEAD - STG_BUFS
           if (has_c && q + C_AHEAD < nq) bulk_wait_read<STG_BUFS - C_AHEAD>();
