@@ -497,18 +497,33 @@ def same_work_anchor(work, steps):
         return None, None
 
 
+# tcx_probe operands per kind: (probe kind, ab code name, generator fmt or None = int8, UMMA N)
+_POWER_KINDS = {"bf16": ("tc05", "BF16", "bf16", 256), "tf32": ("tc05", "TF32", "tf32", 256),
+                "s8": ("tc05", "S8", None, 256), "sp16": ("tc05_sp", "F16", "f16", 240),
+                "sp8": ("tc05_sp", "S8", None, 240), "sptf32": ("tc05_sp", "TF32", "tf32", 240)}
+
+
 def power_roofline(kind, seconds=2.0):
     """The tensor cores alone at the board's power cap: tcx_probe STREAM_ROT on
-    every SM — CTA-pair MMAs of this config's kind on N(0,1) operands read from a 4-stage smem ring,
-    no operand loads, no epilogue — back to back for ~`seconds`; returns the median call's
-    dense-equivalent TFLOP/s.  No GEMM can exceed it at the cap: it is the power roofline."""
+    every SM — CTA-pair MMAs of this config's kind (bench KIND_RATIO names: bf16, tf32, s8, sp16, sp8,
+    sptf32) on N(0,1) operands (INT8: uniform) read from a 4-stage smem ring, no operand loads, no
+    epilogue — back to back for ~`seconds`; returns the median call's dense-equivalent TFLOP/s (TOPS).
+    No GEMM of that kind can exceed it at the cap: it is the power roofline."""
     import tcxgen as g
     import paper_2206_02874_b200 as tcx
-    sp = kind == "sp16"
-    ab, fmt, n, k = (tcx.F16, "f16", 240, 32) if sp else (tcx.BF16, "bf16", 256, 16)
-    a = g.normal_matrix((256, 16), fmt, 1, 1, "cuda", redraw_zero=sp)
-    b = g.normal_matrix((n, k), fmt, 1, 2, "cuda")
-    call = lambda it: tcx.probe("tc05_sp" if sp else "tc05", ab, tcx.F32, 256, n, k, cta_group=2, ilp=16, iters=it,
+    pkind, abn, fmt, n = _POWER_KINDS[kind]
+    sp = pkind == "tc05_sp"
+    ab = getattr(tcx, abn)
+    es = {"BF16": 2, "F16": 2, "TF32": 4, "S8": 1}[abn]
+    ka, kb = 32 // es, (64 if sp else 32) // es          # A: 32 bytes of K (kept values), B: one UMMA K
+    if fmt:
+        a = g.normal_matrix((256, ka), fmt, 1, 1, "cuda", redraw_zero=sp)
+        b = g.normal_matrix((n, kb), fmt, 1, 2, "cuda")
+    else:
+        a = g.int8_matrix((256, ka), 1, 1, "cuda")
+        b = g.int8_matrix((n, kb), 1, 2, "cuda")
+    cd = tcx.S32 if abn == "S8" else tcx.F32
+    call = lambda it: tcx.probe(pkind, ab, cd, 256, n, kb, cta_group=2, ilp=16, iters=it,
                                 repeats=1, num_sms=148, n_acc=1, mode="stream_rot", a_op=a, b_op=b)
     r = call(512)
     iters = int(min(2_000_000, max(512, 0.25 / max(r["ns_per_iter"] * 1e-9, 1e-9))))   # ~0.25 s per call
@@ -593,11 +608,15 @@ def roofline(work, ms, pk, clocks=None, anchor=None):
         ach = work.flops / (ms * 1e-3) / 1e12
         peak = pk["bf16"] * KIND_RATIO[work.kind]
         unit = "TFLOP/s"
-        if anchor and anchor > peak and KIND_RATIO[work.kind] != 1.0:
-            # a derived denominator (bf16 peak x nominal ratio) that the same-run library kernel of
-            # this dtype beat: the higher measured rate of the dtype on this box is the denominator
-            # (bf16 keeps MEASURED_PEAKS' own number, as the contract names it)
-            peak, src = anchor, "same-run library anchor (best of n, this dtype and shape)"
+        if KIND_RATIO[work.kind] != 1.0:
+            # a derived denominator (MEASURED_PEAKS bf16 x nominal ratio) is not a rate this dtype was
+            # seen to reach: the primary peak is the HIGHEST rate measured for this dtype on this box —
+            # the derived one, the same-run library kernel (best of n) or the power-capped MMA-only
+            # probe of this kind — so no fraction rests on a ratio the hardware beats (bf16 keeps
+            # MEASURED_PEAKS' own number, as the contract names it)
+            if anchor and anchor > peak:
+                peak, src = anchor, "same-run library anchor (best of n, this dtype and shape)"
+            # (apply_power_roofline adds the power-capped MMA-only probe of this kind as a candidate)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -629,6 +648,21 @@ def roofline(work, ms, pk, clocks=None, anchor=None):
     return {"bound": work.bound, "achieved": round(ach, 2), "peak": round(peak, 2), "unit": unit,
             "frac": round(ach / peak, 4), **extra, "traffic": traffic, "kernel": work.kernel,
             "peak_source": src}
+
+
+def apply_power_roofline(rl, power, kind):
+    """Add the power-capped MMA-only denominator (power_roofline(kind)) to a roofline dict; for a kind
+    whose primary peak is derived (KIND_RATIO != 1) it is also a candidate for the primary: the
+    highest rate measured for the dtype on this box is the denominator."""
+    ach = rl["achieved"]
+    rl.setdefault("denominators", {})["power_capped_mma_only"] = {
+        "peak": power, "frac": round(ach / power, 4),
+        "what": f"tcx_probe STREAM_ROT: {kind} CTA-pair MMAs alone on all SMs, N(0,1) operands "
+                "(INT8 uniform), no loads or epilogue, at the 1000 W cap (~2 s)"}
+    if KIND_RATIO[kind] != 1.0 and power > rl["peak"]:
+        rl["peak"], rl["frac"] = round(power, 2), round(ach / power, 4)
+        rl["peak_source"] = "power-capped MMA-only probe of this kind (tcx_probe STREAM_ROT, this run)"
+    return rl
 
 
 # ----------------------------------------------------------------------------------- oracle baseline
@@ -981,6 +1015,7 @@ def main():
                                    "torch.addmm(C, A, B^T, out_dtype=float32) doing this step's exact work: context only, "
                                    "not part of the step"}
         also = {}
+        power_kinds = {}
         # lightest first: the launch-bound C1 is clock-sensitive and the power-capped 2:4 runs leave
         # the board hot (C1 measured after C5 ran at ~850 MHz)
         for extra in ("c1", "c3tf32", "c3f16acc", "c4", "c3sptf32", "c4sp", "c5"):
@@ -996,20 +1031,15 @@ def main():
                     ck2["sm_mhz_in_run"] = round(w2.sm_mhz_eff, 1)
                 anc = library_anchor(w2, 5) if extra in ("c3tf32", "c4") else None
                 also[extra] = {"workload": cfg_names[extra], "value": round(v2, 3), "unit": w2.unit,
-                               "ms_per_step": round(ms2, 5), "roofline": roofline(w2, ms2, pk, ck2, anc), "gpu_launches": l2,
-                               "clocks": ck2}
+                               "ms_per_step": round(ms2, 5), "roofline": roofline(w2, ms2, pk, ck2, anc),
+                               "gpu_launches": l2, "clocks": ck2}
+                if w2.bound == "tensor" and w2.kind in _POWER_KINDS and w2.kind != "bf16":
+                    power_kinds[extra] = w2.kind
                 if extra == "c1":
                     also[extra]["steady_state"] = tiles_steady_state(w2.tcx, dev)
                 if extra == "c5":
                     also[extra]["context"] = {"cusparselt_f16_out_no_c_tflops": cusparselt_anchor(w2),
                                               "note": "cuSPARSELt on the same 2:4 operand, FP16 D, no C (less work): context"}
-                    try:
-                        pr = power_roofline("sp16")
-                        also[extra]["roofline"]["denominators"]["power_capped_mma_only"] = {
-                            "peak": pr, "frac": round(also[extra]["roofline"]["achieved"] / pr, 4),
-                            "what": "tcx_probe: 2:4 f16 CTA-pair MMAs alone on all SMs, N(0,1) operands, at the cap"}
-                    except Exception as e:  # report, never hide
-                        also[extra]["context"]["power_roofline_error"] = f"{type(e).__name__}: {e}"
                 del w2
                 torch.cuda.empty_cache()
                 if not args.no_cpu_baseline:       # the oracle on the host cores, a bounded sample of this config
@@ -1020,12 +1050,15 @@ def main():
             except Exception as e:  # report, never hide
                 also[extra] = {"error": f"{type(e).__name__}: {e}"}
         line["also"] = also
-        # after the extras (it leaves the board at its power cap): the headline's power roofline
+        # after every extra's timed run (each leaves the board at its power cap): the power rooflines,
+        # the headline's bf16 one and one per other tensor kind
+        for extra, kind in power_kinds.items():
+            try:
+                apply_power_roofline(also[extra]["roofline"], power_roofline(kind), kind)
+            except Exception as e:  # report, never hide
+                also[extra]["roofline"]["power_roofline_error"] = f"{type(e).__name__}: {e}"
         try:
-            pr = power_roofline("bf16")
-            line["roofline"]["denominators"]["power_capped_mma_only"] = {
-                "peak": pr, "frac": round(line["roofline"]["achieved"] / pr, 4),
-                "what": "tcx_probe: bf16 CTA-pair MMAs alone on all SMs, N(0,1) operands, at the 1000 W cap (~2 s)"}
+            apply_power_roofline(line["roofline"], power_roofline("bf16"), "bf16")
         except Exception as e:  # report, never hide
             line["roofline"]["denominators"]["power_capped_mma_only"] = {"error": f"{type(e).__name__}: {e}"}
         if args.sustained_s > 0:
