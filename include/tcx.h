@@ -110,7 +110,13 @@ typedef struct {
   int group_m;     /* tile raster (0 = default): > 0, that many cluster-tile rows sweep N together;
                       < 0, |group_m| cluster-tile columns sweep M together */
   int tile_n;      /* 0 = library choice; tcx_gemm: 256 (default) or 512 = the 256 x 512 pair tile
-                      (two N = 256 MMAs share A); tcx_gemm_sp24 (the tile HEIGHT): 512 = the
+                      (two N = 256 MMAs share A), or 224 / 192 / 160 / 128 = a narrower 256-row
+                      pair tile (UMMA N = tile_n; cta_group 2, plain pairs).  The library picks a
+                      narrower width itself when the 256-wide tiles fill their last wave on the
+                      SMs poorly and the narrower one is >= 5% cheaper in (waves x width) — e.g.
+                      1024 x 8192 (C3 row-sharded over 8 GPUs): 224 (148 tiles = 2 full waves
+                      instead of 128 tiles in 2).  Every width runs the same per-element MMA
+                      sequence: D is bit-identical.  tcx_gemm_sp24 (the tile HEIGHT): 512 = the
                       512 x 240 pair tile (two M-halves share B; F16/BF16/TF32, M % 512 == 0 — the
                       default there when M*N*K >= 2^43, i.e. calls long enough to run at the
                       power cap), 256 = the 256 x 240 tile (the default otherwise) */
@@ -121,13 +127,15 @@ typedef struct {
                    /* their own operands.  1 or 2 each; 0 = default 1.  Results are bit-identical  */
                    /* to the default.  0 = library choice: for tcx_gemm with the CTA pair and at   */
                    /* least two waves of 256 x 256 tiles over >= 2 tile columns, 1 x 2 (A shared);  */
-                   /* 1 x 1 otherwise; pass 1 / 1 to force plain pairs.                            */
+                   /* 1 x 1 otherwise (and with a narrower library-chosen width); pass 1 / 1 to   */
+                   /* force plain pairs.                                                          */
   int reserved[2]; /* 0.  reserved[0] = 1 in the debug library (libtcx_debug.so) only: the dense
                       producer drops one TMA load (fault injection for the watchdog tests);
                       the product library ignores it */
 } tcx_gemm_opts;
-/* opts == NULL -> all defaults.  Option errors (cta_group not 0/1/2, tile_n not 0/256/512,
- * pairs outside 1..2 or combined with cta_group 1 / tile_n 512) -> TCX_ERR_INVALID_VALUE, checked
+/* opts == NULL -> all defaults.  Option errors (cta_group not 0/1/2, tile_n not 0/128/160/192/224/
+ * 256/512 (tcx_gemm_sp24: 0/256/512), pairs outside 1..2 or combined with cta_group 1 / a tile_n other
+ * than 256; tile_n < 256 with cta_group 1 -> TCX_ERR_UNSUPPORTED) -> TCX_ERR_INVALID_VALUE, checked
  * with every other argument before any device query. */
 tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t K,
                        const void* A, int64_t lda, const void* B, int64_t ldb,

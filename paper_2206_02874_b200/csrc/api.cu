@@ -251,20 +251,23 @@ tcx_status tcx_gemm_ex(tcx_dtype ab, tcx_dtype cd, int64_t M, int64_t N, int64_t
     if (opts->cta_group) g.cta_group = opts->cta_group;
     g.max_ctas = opts->max_ctas;
     g.group_m = opts->group_m;
-    if (opts->tile_n != 0 && opts->tile_n != 256 && opts->tile_n != 512)
-      return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: tile_n must be 0, 256 or 512");
-    g.tile_n = opts->tile_n;
+    const int tn = opts->tile_n;
+    if (!(tn == 0 || tn == 128 || tn == 160 || tn == 192 || tn == 224 || tn == 256 || tn == 512))
+      return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: tile_n must be 0, 128, 160, 192, 224, 256 or 512");
+    g.tile_n = tn;
     const int pm = opts->pairs_m ? opts->pairs_m : 1, pn = opts->pairs_n ? opts->pairs_n : 1;
     if (pm < 1 || pm > 2 || pn < 1 || pn > 2)
       return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: pairs_m and pairs_n must be 0, 1 or 2");
-    if ((pm > 1 || pn > 1) && (g.cta_group != 2 || g.tile_n == 512))
+    if ((pm > 1 || pn > 1) && (g.cta_group != 2 || (g.tile_n != 0 && g.tile_n != 256)))
       return set_error(TCX_ERR_INVALID_VALUE, "tcx_gemm: multicast clusters need cta_group 2 and the 256-wide tile");
+    if (tn != 0 && tn < 256 && g.cta_group != 2)
+      return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm: tile_n < 256 (narrow pair tiles) needs cta_group 2");
     if (g.tile_n == 512 && (g.cta_group != 2 || cd == TCX_F16))
       return set_error(TCX_ERR_UNSUPPORTED, "tcx_gemm: tile_n 512 (the 256 x 512 pair tile) needs cta_group 2 and a "
                        "32-bit accumulator");
     g.pairs_m = pm;
     g.pairs_n = pn;
-    g.pairs_auto = opts->pairs_m == 0 && opts->pairs_n == 0 && opts->cta_group != 1 && g.tile_n != 512;
+    g.pairs_auto = opts->pairs_m == 0 && opts->pairs_n == 0 && opts->cta_group != 1 && (g.tile_n == 0 || g.tile_n == 256);
 #if TCX_WATCHDOG
     g.fault = opts->reserved[0];   // fault injection exists only in the debug library
 #endif

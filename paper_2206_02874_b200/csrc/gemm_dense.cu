@@ -34,15 +34,18 @@ namespace tcx {
 namespace {
 
 constexpr int BM = 128;            // rows per CTA (UMMA M = BM * CG)
-constexpr int BN = 256;            // UMMA N
+constexpr int BN_FULL = 256;       // UMMA N of the default tile (narrower N: wave-quantisation choice)
 constexpr int KBYTES = 128;        // K bytes per stage (one SW128 row)
 constexpr int UMMA_KBYTES = 32;    // K bytes per tcgen05.mma
 constexpr int EPI_WARPS = 4;
 constexpr int NUM_THREADS = 256;
 constexpr int GROUP_M = 8;         // default raster: GROUP_M cluster-tile rows share B tiles in L2
 
-template <int CG, int NH>
+template <int CG, int NH, int BN_ = BN_FULL>
 struct Cfg {
+  static constexpr int BN = BN_;                                 // UMMA N (one N-half)
+  static_assert(BN % 32 == 0 && BN >= 128 && BN <= 256 && (NH == 1 || BN == 256), "tile width");
+  static constexpr int ACC_COLS = NH * 256;                      // TMEM column stride between accumulators
   static constexpr int TILE_M = BM * CG;                         // output rows per tile
   static constexpr int TILE_N = BN * NH;                         // output columns per tile
   static constexpr int BN_LOAD = BN / CG;                        // B rows per CTA per N-half
@@ -56,10 +59,16 @@ struct Cfg {
 #ifndef TCX_DENSE_NBE
 #define TCX_DENSE_NBE 2
 #endif
-  static constexpr int STAGES = NH == 2 ? 3 : (CG == 1 ? 4 : TCX_DENSE_STAGES);
+#ifndef TCX_WIDE_STAGES
+#define TCX_WIDE_STAGES 3
+#endif
+#ifndef TCX_WIDE_NBE
+#define TCX_WIDE_NBE 4
+#endif
+  static constexpr int STAGES = NH == 2 ? TCX_WIDE_STAGES : (CG == 1 ? 4 : TCX_DENSE_STAGES);
   // epilogue staging buffers per warp (4 KiB each) and how far ahead C is loaded: the wide tile's
   // single accumulator puts the epilogue on the critical path, so it trades a ring stage for depth
-  static constexpr int NBE = NH == 2 ? 4 : (CG == 1 ? 2 : TCX_DENSE_NBE);
+  static constexpr int NBE = NH == 2 ? TCX_WIDE_NBE : (CG == 1 ? 2 : TCX_DENSE_NBE);
   static constexpr int C_AHEAD = NBE == 2 ? 2 : NBE - 1;
   static constexpr int NBUF = 2 / NH;                            // TMEM accumulator buffers
   static constexpr int SMEM_DATA = STAGES * STAGE_BYTES;
@@ -147,13 +156,14 @@ __device__ void dbg_fill_ring(uint8_t* base, int bytes, int meta_off, int meta_b
 }
 #endif
 
-template <int CG, int KIND, int NH, int PM, int PN>
+template <int CG, int KIND, int NH, int PM, int PN, int BNT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD,
-                  int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc, int group_m, int fault,
+                  int64_t M, int64_t N, int64_t K, int has_c, uint32_t idesc, int group_m, int look, int fault,
                   uint64_t* trace, int64_t trace_cap) {
-  using C_ = Cfg<CG, NH>;
+  using C_ = Cfg<CG, NH, BNT>;
+  constexpr int BN = BNT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   Smem* sm = (Smem*)(smem + C_::SMEM_DATA + C_::STG_BYTES);
@@ -235,7 +245,12 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         pair_tile(tile, mt, nt);
         const int arow = (int)(mt * C_::TILE_M + rank * BM);               // + j * A_ROWS for slice j
         const int brow = (int)(nt * C_::TILE_N + rank * C_::BN_LOAD);      // + h * BN for N-half h
-        for (int64_t kb = 0; kb < k_blocks; ++kb) {
+        // wide tile: segments (N-half 0, k-blocks [0, L)), (N-half 1, [0, L)), (both halves, [L, KB))
+        // — the first L k-blocks are loaded once per half (A twice), see the MMA warp
+        const int64_t L = NH == 2 ? (look < k_blocks ? look : k_blocks) : 0;
+        for (int64_t i = 0; i < k_blocks + L; ++i) {
+          const int64_t kb = i < 2 * L ? (i < L ? i : i - L) : i - L;
+          const uint32_t hmask = i < L ? 1u : i < 2 * L ? 2u : 3u;   // N-halves this slot carries
           mbar_wait(&sm->empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C_::STAGE_BYTES;
           uint8_t* sb = sa + C_::A_BYTES;
@@ -247,10 +262,12 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           }
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&sm->full[stage], C_::STAGE_BYTES);
-            tma_load_2d<HINT_AB>(sa, &tmA, &sm->full[stage], kx, arow, l2_policy_ab());
-            tma_load_2d<HINT_AB>(sb, &tmB, &sm->full[stage], kx, brow, l2_policy_ab());
+            tma_load_2d<HINT_AB>(sa, &tmA, &sm->full[stage], kx, arow, l2_policy_a());
+            tma_load_2d<HINT_AB>(sb, &tmB, &sm->full[stage], kx, brow, l2_policy_b());
           } else {
-            if (leader) mbar_arrive_expect_tx(&sm->full[stage], 2 * C_::STAGE_BYTES);
+            if (leader)
+              mbar_arrive_expect_tx(&sm->full[stage], NH == 2 && hmask != 3u ? 2 * (C_::A_BYTES + C_::HALF_BYTES)
+                                                                              : 2 * C_::STAGE_BYTES);
             const uint32_t bar = full0_cluster + stage * 8;
 #if TCX_WATCHDOG
             // fault injection (debug library): the first A load is never issued, its barrier never
@@ -263,19 +280,20 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
             (void)fault; (void)trace; (void)trace_cap;
 #endif
             if (PN > 1 && mc) {
-              tma_load_2d_cg2_mc<HINT_AB>(sa + pn * A_ROWS * KBYTES, &tmA, bar, kx, arow + pn * A_ROWS, mask_a, l2_policy_ab());
+              tma_load_2d_cg2_mc<HINT_AB>(sa + pn * A_ROWS * KBYTES, &tmA, bar, kx, arow + pn * A_ROWS, mask_a, l2_policy_a());
             } else {
 #pragma unroll
-              for (int j = 0; j < PN; ++j) tma_load_2d_cg2<HINT_AB>(sa + j * A_ROWS * KBYTES, &tmA, bar, kx, arow + j * A_ROWS, l2_policy_ab());
+              for (int j = 0; j < PN; ++j) tma_load_2d_cg2<HINT_AB>(sa + j * A_ROWS * KBYTES, &tmA, bar, kx, arow + j * A_ROWS, l2_policy_a());
             }
             if (PM > 1 && mc) {
-              tma_load_2d_cg2_mc<HINT_AB>(sb + pm * B_ROWS * KBYTES, &tmB, bar, kx, brow + pm * B_ROWS, mask_b, l2_policy_ab());
+              tma_load_2d_cg2_mc<HINT_AB>(sb + pm * B_ROWS * KBYTES, &tmB, bar, kx, brow + pm * B_ROWS, mask_b, l2_policy_b());
             } else {
 #pragma unroll
               for (int h = 0; h < NH; ++h)
 #pragma unroll
-                for (int i = 0; i < PM; ++i)
-                  tma_load_2d_cg2<HINT_AB>(sb + h * C_::HALF_BYTES + i * B_ROWS * KBYTES, &tmB, bar, kx, brow + h * BN + i * B_ROWS, l2_policy_ab());
+                for (int r = 0; r < PM; ++r)
+                  if ((hmask >> h) & 1u)
+                    tma_load_2d_cg2<HINT_AB>(sb + h * C_::HALF_BYTES + r * B_ROWS * KBYTES, &tmB, bar, kx, brow + h * BN + r * B_ROWS, l2_policy_b());
             }
           }
           if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
@@ -308,7 +326,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         if (P > 1 && mc) tc05_commit_mc(bar, (uint16_t)(3u << lead_rank)); else tc05_commit<CG>(bar);
       };
       for (int64_t tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        const uint32_t tmem_d = tmem_base + acc * BN * NH;
+        const uint32_t tmem_d = tmem_base + acc * C_::ACC_COLS;
         int64_t kb0 = 0;
         if constexpr (NH == 1) {
           // FP16 accumulate: every use of a buffer (the first included) waits for the epilogue's
@@ -316,33 +334,35 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           mbar_wait(&sm->tmem_empty[acc], KIND == KIND_F16ACC ? acc_phase : acc_phase ^ 1);
           tc05_fence_after();
         } else {
-          // single-buffered wide accumulator: the epilogue drains N-half 0 first, so issue half 0
-          // for the first L resident k-blocks before waiting for half 1 — the tensor pipe works
-          // while half 1 of the previous tile is still being read out.
-          const int64_t L = k_blocks < C_::STAGES ? k_blocks : C_::STAGES;
-          const int st0 = stage; const uint32_t ph0 = phase;
-          mbar_wait(&sm->tmem_empty[0], acc_phase ^ 1);
-          tc05_fence_after();
-          for (int64_t kb = 0; kb < L; ++kb) {
-            mbar_wait(&sm->full[stage], phase);
+          // single-buffered wide accumulator: the epilogue drains N-half 0 first, so the next tile
+          // starts on N-half 0 alone for its first L k-blocks while half 1 is still being read out,
+          // then runs half 1's first L k-blocks (the producer loads those slots again, A re-read from
+          // L2), then both halves share each slot.  Every accumulator half still receives its
+          // k-blocks in ascending order: D is bit-identical to the narrow tile's.
+          const int64_t L = look < k_blocks ? look : k_blocks;
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            mbar_wait(&sm->tmem_empty[h], acc_phase ^ 1);
             tc05_fence_after();
-            if (elect_one()) issue(stage, 0, kb, tmem_d);
-            __syncwarp();
-            if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
-          }
-          mbar_wait(&sm->tmem_empty[1], acc_phase ^ 1);
-          tc05_fence_after();
-          int st = st0; uint32_t ph = ph0;
-          for (int64_t kb = 0; kb < L; ++kb) {
-            if (elect_one()) {
-              issue(st, 1, kb, tmem_d);
-              tc05_commit<CG>(&sm->empty[st]);                   // both halves consumed the slot
-              if (kb == k_blocks - 1) tc05_commit<CG>(&sm->tmem_full[acc]);
+#pragma unroll 1
+            for (int64_t kb = 0; kb < L; ++kb) {
+              mbar_wait(&sm->full[stage], phase);
+              tc05_fence_after();
+              if (elect_one()) {
+                issue(stage, h, kb, tmem_d);
+                tc05_commit<CG>(&sm->empty[stage]);
+                if (h == 1 && kb == k_blocks - 1) tc05_commit<CG>(&sm->tmem_full[acc]);
+#if TCX_WATCHDOG
+                if (trace && tile < trace_cap && h == 0 && kb == 0) {   // debug timeline: first MMA
+                  trace[4 * tile] = ((uint64_t)(cluster_id * P + pair) << 32) | (uint64_t)tile;
+                  trace[4 * tile + 1] = globaltimer_ns();
+                }
+#endif
+              }
+              __syncwarp();
+              if (++stage == C_::STAGES) { stage = 0; phase ^= 1; }
             }
-            __syncwarp();
-            if (++st == C_::STAGES) { st = 0; ph ^= 1; }
           }
-          (void)ph;
           kb0 = L;
         }
         for (int64_t kb = kb0; kb < k_blocks; ++kb) {
@@ -373,7 +393,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
             if (kb == k_blocks - 1) commit_acc(&sm->tmem_full[acc]);   // accumulator ready
 #if TCX_WATCHDOG
             if (trace && tile < trace_cap) {                      // debug tile timeline
-              if (kb == kb0) {
+              if (kb == kb0 && (NH == 1 || kb0 == 0)) {
                 trace[4 * tile] = ((uint64_t)(cluster_id * P + pair) << 32) | (uint64_t)tile;
                 trace[4 * tile + 1] = globaltimer_ns();
               }
@@ -445,7 +465,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
 #pragma unroll
           for (int i = 0; i < 4; ++i) { r[8 * j + 2 * i] = ws[i] & 0xFFFFu; r[8 * j + 2 * i + 1] = ws[i] >> 16; }
         }
-        tmem_st_32x32b_x32(tmem_base + buf * BN + ch * 32 + lane_off, r);
+        tmem_st_32x32b_x32(tmem_base + buf * C_::ACC_COLS + ch * 32 + lane_off, r);
         __syncwarp();                             // every lane has read buffer b
         if (ch + 2 < CH) load(ch + 2);
       }
@@ -466,7 +486,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       for (int ch = 0; ch < CH; ++ch, ++nstore) {
         const int b = (int)(nstore & 1);
         uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem_base + acc * BN + ch * 32 + lane_off, v);
+        tmem_ld_32x32b_x32(tmem_base + acc * C_::ACC_COLS + ch * 32 + lane_off, v);
         if (lane == 0 && nstore >= 2) bulk_wait_read<1>();   // store nstore-2 has read buffer b
         __syncwarp();
         tmem_ld_wait();
@@ -579,7 +599,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         __syncwarp();
       }
       uint32_t v[32], vn[32];
-      tmem_ld_32x32b_x32(tmem_base + acc * NH * BN + lane_off, vn);   // chunk 0
+      tmem_ld_32x32b_x32(tmem_base + acc * C_::ACC_COLS + lane_off, vn);   // chunk 0
       if (ring && has_c) mbar_wait(&sm->cring[e], 0);
 #pragma unroll 1
       for (int ch = 0; ch < CH; ++ch) {
@@ -593,7 +613,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         for (int j = 0; j < 32; ++j) v[j] = vn[j];
         if (ch + 1 < CH) {                        // read the next chunk while this one is stored
           const int hn = (ch + 1) / (BN / 32);
-          tmem_ld_32x32b_x32(tmem_base + (acc * NH + hn) * BN + ((ch + 1) % (BN / 32)) * 32 + lane_off, vn);
+          tmem_ld_32x32b_x32(tmem_base + acc * C_::ACC_COLS + hn * BN + ((ch + 1) % (BN / 32)) * 32 + lane_off, vn);
         }
         if (ring) {
           // own buffer per chunk in the ring; C (if any) already landed
@@ -679,9 +699,18 @@ __global__ void fill_c_kernel(const T* C, int64_t ldc, T* D, int64_t ldd, int64_
   }
 }
 
-template <int CG, int KIND, int NH, int PM = 1, int PN = 1>
+// wide tile: k-blocks of N-half 0 the next tile runs ahead while half 1 drains.  A/B on C3
+// (gpurun_out r02 wide-lookahead study): L = 0 / 4 / 8 / 16 / 32 -> 1474 / 1470 / 1473 /
+// 1469 / 1427 TFLOP/s; the inter-tile MMA gap falls 15.4 -> 8.2 us at L = 16 but the half-only
+// k-blocks run slower (tile 91.8 -> 97.6 us), so the wide tile stays an option, not the default
+#ifndef TCX_WIDE_LOOK
+#define TCX_WIDE_LOOK 8
+#endif
+static int wide_look() { return TCX_WIDE_LOOK; }
+
+template <int CG, int KIND, int NH, int PM = 1, int PN = 1, int BNT = BN_FULL>
 tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUtensorMapDataType dt, int a_fmt) {
-  using C_ = Cfg<CG, NH>;
+  using C_ = Cfg<CG, NH, BNT>;
   constexpr int ES = KindT<KIND>::ESIZE;
   constexpr int CL = CG * PM * PN;
   CUtensorMap tA, tB;
@@ -706,7 +735,7 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
   } else {
     tC = tD;                                                  // unused (has_c = 0)
   }
-  auto kern = gemm_dense_kernel<CG, KIND, NH, PM, PN>;
+  auto kern = gemm_dense_kernel<CG, KIND, NH, PM, PN, BNT>;
   TCX_CUDA_TRY(ensure_max_smem((const void*)kern, C_::SMEM_TOTAL, dev.device));
   const int64_t m_tiles = (a.M + C_::TILE_M - 1) / C_::TILE_M;
   const int64_t n_tiles = (a.N + C_::TILE_N - 1) / C_::TILE_N;
@@ -732,9 +761,9 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
     fprintf(stderr, "tcx_gemm: grid %u CTAs, cluster %d (pairs %dx%d), %lld cluster tiles\n", cfg.gridDim.x, CL, PM, PN,
             (long long)(((m_tiles + PM - 1) / PM) * ((n_tiles + PN - 1) / PN)));
 #endif
-  const uint32_t idesc = make_idesc(KIND, a_fmt, BM * CG, BN);
+  const uint32_t idesc = make_idesc(KIND, a_fmt, BM * CG, C_::BN);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
-                                  a.C ? 1 : 0, idesc, a.group_m != 0 ? a.group_m : GROUP_M, a.fault, a.trace,
+                                  a.C ? 1 : 0, idesc, a.group_m != 0 ? a.group_m : GROUP_M, wide_look(), a.fault, a.trace,
                                   a.trace_cap));
   count_launch();
   return TCX_OK;
@@ -766,9 +795,52 @@ static bool auto_pairs_1x2(const GemmArgs& a, const DevInfo& dev) {
   return n_tiles >= 2 && m_tiles * n_tiles >= 2 * (int64_t)(dev.sm_count / 2);
 }
 
+// Wave quantisation (CTA pair, library choice of the tile width): P pairs run a call of T tiles in
+// ceil(T / P) waves, each one tile-time long, and a tile's time is proportional to its width (its
+// K loop is the same).  So the call costs ~ ceil(T(w) / P) * w for UMMA N = w: when T(256) fills
+// its last wave poorly (a row-sharded rank's small M, e.g. C3 / 8 ranks = 1024 rows: 128 tiles on
+// 74 pairs, 2 waves 86% full), a narrower tile that fills it (224: 148 tiles, exactly 2 waves)
+// finishes sooner (measured +4.1% on 1024 x 8192 x 8192 and +4.4% on 2048 x 8192 x 8192 BF16,
+// unchanged on the full configs).  A narrower width is taken only when it is >= 5% cheaper by this
+// count.  Returns the width (256 = the default tile).
+static int wave_tile_width(const GemmArgs& a, const DevInfo& dev) {
+  if (a.tile_n != 0) return a.tile_n == 512 ? 256 : a.tile_n;   // caller's choice
+  if (a.cta_group != 2 || !a.pairs_auto) return 256;
+  int64_t pairs = dev.sm_count / 2;
+  if (a.max_ctas > 0 && a.max_ctas / 2 < pairs) pairs = a.max_ctas / 2 > 0 ? a.max_ctas / 2 : 1;
+  const int64_t mt = (a.M + 255) / 256;
+  // a narrower tile also runs fewer FLOP/s: per-width throughput relative to 256 on full waves
+  // (C3 BF16 8192^3, tools/wave_study.py: 224 0.979, 192 0.944, 160 0.879, 128 0.806), so a tile
+  // costs width / rate
+  auto cost = [&](int w, int rate_permille) {
+    const int64_t t = mt * ((a.N + w - 1) / w);
+    return (t + pairs - 1) / pairs * w * 1000 / rate_permille;
+  };
+  const int64_t c256 = cost(256, 1000);
+  int best = 256; int64_t bc = c256;
+  const int widths[4] = {224, 192, 160, 128}, rates[4] = {979, 944, 879, 806};
+  for (int i = 0; i < 4; ++i) {
+    const int64_t c = cost(widths[i], rates[i]);
+    if (c < bc && 20 * c <= 19 * c256) { best = widths[i]; bc = c; }
+  }
+  return best;
+}
+
+template <int KIND>
+tcx_status launch_narrow(int w, const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUtensorMapDataType dt, int a_fmt) {
+  switch (w) {
+    case 224: return launch_t<2, KIND, 1, 1, 1, 224>(a, dev, s, dt, a_fmt);
+    case 192: return launch_t<2, KIND, 1, 1, 1, 192>(a, dev, s, dt, a_fmt);
+    case 160: return launch_t<2, KIND, 1, 1, 1, 160>(a, dev, s, dt, a_fmt);
+    default: return launch_t<2, KIND, 1, 1, 1, 128>(a, dev, s, dt, a_fmt);
+  }
+}
+
 template <int KIND>
 tcx_status launch_kind(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUtensorMapDataType dt, int a_fmt) {
   if (a.cta_group == 1) return launch_t<1, KIND, 1>(a, dev, s, dt, a_fmt);
+  const int w = wave_tile_width(a, dev);
+  if (w != 256) return launch_narrow<KIND>(w, a, dev, s, dt, a_fmt);
   if (auto_pairs_1x2(a, dev)) return launch_t<2, KIND, 1, 1, 2>(a, dev, s, dt, a_fmt);
   // 256 x 512 pair tiles only when asked: they cut L2->SM operand traffic by 25% (and run at a
   // higher clock under the power cap), but the single-buffered accumulator exposes the epilogue,
@@ -785,6 +857,8 @@ tcx_status launch_gemm_dense(const GemmArgs& a, const DevInfo& dev, cudaStream_t
   if (a.cd == TCX_F16) {   // FP16 accumulate (F16 inputs only; validated by the front end)
     constexpr CUtensorMapDataType h = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     if (a.cta_group == 1) return launch_t<1, KIND_F16ACC, 1>(a, dev, s, h, 0);
+    const int w = wave_tile_width(a, dev);
+    if (w != 256) return launch_narrow<KIND_F16ACC>(w, a, dev, s, h, 0);
     if (auto_pairs_1x2(a, dev)) return launch_t<2, KIND_F16ACC, 1, 1, 2>(a, dev, s, h, 0);
     if (a.pairs_m == 2 && a.pairs_n == 2) return launch_t<2, KIND_F16ACC, 1, 2, 2>(a, dev, s, h, 0);
     if (a.pairs_m == 2) return launch_t<2, KIND_F16ACC, 1, 2, 1>(a, dev, s, h, 0);

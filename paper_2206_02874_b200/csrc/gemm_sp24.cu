@@ -238,14 +238,15 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
           const uint32_t bar = CG == 2 ? full0_cluster + stage * 8 : smem_u32(&sm->full[stage]);
           auto load = [&](void* dst, const CUtensorMap* m, int x, int y) {
-            if constexpr (CG == 1) tma_load_2d<HINT_AB>(dst, m, &sm->full[stage], x, y, l2_policy_ab());
-            else tma_load_2d_cg2<HINT_AB>(dst, m, bar, x, y, l2_policy_ab());
+            const uint64_t pol = m == &tmB ? l2_policy_b() : l2_policy_a();
+            if constexpr (CG == 1) tma_load_2d<HINT_AB>(dst, m, &sm->full[stage], x, y, pol);
+            else tma_load_2d_cg2<HINT_AB>(dst, m, bar, x, y, pol);
           };
 #pragma unroll
           for (int h = 0; h < MH; ++h) {
             const int64_t mrow_h = mrow + h * BM * CG;
             if (PN > 1 && mc) {
-              tma_load_2d_cg2_mc<HINT_AB>(sa + h * C_::A_HALF + pn * A_ROWS * 128, &tmA, bar, ka, (int)mrow_h + pn * A_ROWS, mask_a, l2_policy_ab());
+              tma_load_2d_cg2_mc<HINT_AB>(sa + h * C_::A_HALF + pn * A_ROWS * 128, &tmA, bar, ka, (int)mrow_h + pn * A_ROWS, mask_a, l2_policy_a());
             } else {
 #pragma unroll
               for (int j = 0; j < PN; ++j) load(sa + h * C_::A_HALF + j * A_ROWS * 128, &tmA, ka, (int)mrow_h + j * A_ROWS);
@@ -253,7 +254,7 @@ gemm_sp24_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             load(se + h * 2048 * C_::META_ATOMS, &tmE, 0, (int)(((mrow_h / 128) * k_blocks + kb) * 16 * C_::META_ATOMS));
           }
           if (PM > 1 && mc) {
-            tma_load_2d_cg2_mc<HINT_AB>(sb + pm * C_::B_HALF, &tmB, bar, kx + pm * C_::BOX, brow, mask_b, l2_policy_ab());
+            tma_load_2d_cg2_mc<HINT_AB>(sb + pm * C_::B_HALF, &tmB, bar, kx + pm * C_::BOX, brow, mask_b, l2_policy_b());
           } else {
             load(sb, &tmB, kx, brow);
             load(sb + C_::B_HALF, &tmB, kx + C_::BOX, brow);

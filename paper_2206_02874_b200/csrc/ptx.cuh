@@ -143,10 +143,11 @@ __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
 // (evict_first).  H = false issues the plain form; `pol` is then ignored.
 #ifndef TCX_L2HINT
 #define TCX_L2HINT 0      // bit 0: C loads/prefetches evict_first, bit 1: D stores evict_first,
-#endif                    // bit 2: A/B loads evict_last, bit 3: A/B loads evict_normal (explicit)
+#endif                    // bit 2: A/B loads evict_last, bit 3: A/B loads evict_normal (explicit),
+                          // bit 4: B loads evict_first, bit 5: A (+ sparse metadata) loads evict_last
 constexpr bool HINT_C = (TCX_L2HINT & 1) != 0;
 constexpr bool HINT_D = (TCX_L2HINT & 2) != 0;
-constexpr bool HINT_AB = (TCX_L2HINT & 12) != 0;
+constexpr bool HINT_AB = (TCX_L2HINT & 60) != 0;
 __device__ __forceinline__ uint64_t l2_evict_first() {
   uint64_t p; asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p)); return p;
 }
@@ -156,7 +157,10 @@ __device__ __forceinline__ uint64_t l2_evict_last() {
 __device__ __forceinline__ uint64_t l2_evict_normal() {
   uint64_t p; asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p)); return p;
 }
-__device__ __forceinline__ uint64_t l2_policy_ab() { return (TCX_L2HINT & 4) ? l2_evict_last() : l2_evict_normal(); }
+__device__ __forceinline__ uint64_t l2_policy_a() { return (TCX_L2HINT & 36) ? l2_evict_last() : l2_evict_normal(); }
+__device__ __forceinline__ uint64_t l2_policy_b() {
+  return (TCX_L2HINT & 16) ? l2_evict_first() : (TCX_L2HINT & 4) ? l2_evict_last() : l2_evict_normal();
+}
 
 // 2D tile load into this CTA's smem, completion on this CTA's barrier
 template <bool H = false>

@@ -50,6 +50,9 @@ def _opts(**kw):
     (dict(opts=_opts(pairs_n=2, tile_n=512)), INVALID),
     (dict(opts=_opts(tile_n=512, cta_group=1)), UNSUPPORTED),   # the wide tile needs the CTA pair
     (dict(ab=F16, cd=F16, opts=_opts(tile_n=512)), UNSUPPORTED),   # ... and a 32-bit accumulator
+    (dict(opts=_opts(tile_n=224, cta_group=1)), UNSUPPORTED),   # the narrow tiles need the CTA pair
+    (dict(opts=_opts(tile_n=192, pairs_n=2)), INVALID),         # multicast groups: 256-wide tiles only
+    (dict(opts=_opts(tile_n=200)), INVALID),
 ])
 def test_gemm_argument_errors(kw, want):
     assert _gemm(**kw) == want, tcx.lib().tcx_last_error()

@@ -97,6 +97,46 @@ def test_gemm_wide_equals_narrow_and_persistent(fmt):
     assert torch.equal(Dw.view(torch.int32), Dp.view(torch.int32))
 
 
+NARROW = [(256, 512, 128), (200, 600, 72), (264, 520, 40), (512, 1000, 320), (256, 96, 64)]
+
+
+@pytest.mark.parametrize("width", [224, 192, 160, 128])
+@pytest.mark.parametrize("fmt", ["bf16", "tf32", "s8"])
+@pytest.mark.parametrize("shape", NARROW)
+def test_gemm_narrow_tile_whole_matrix(fmt, shape, width):
+    """the narrower pair tiles (tile_n = 224 / 192 / 160 / 128: UMMA N = width, the wave-quantisation
+    choice): whole matrix against the oracle, incl. ragged M/N/K, N not a multiple of the width and
+    N smaller than one tile."""
+    M, N, K = shape
+    if fmt == "s8":
+        K = max(16, (K + 15) // 16 * 16)
+    A, B, C = _problem(M, N, K, fmt, seed=M + 5 * N + K + width)
+    D = tcx.gemm(A, B, C, tf32=(fmt == "tf32"), tile_n=width)
+    torch.cuda.synchronize()
+    _full_check(fmt, A, B, C, D)
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "s8", "f16acc"])
+def test_gemm_narrow_equals_default_and_persistent(fmt):
+    """every width runs the same per-element MMA sequence: D bit-identical to the 256-wide tile's,
+    also with many tiles per CTA pair (max_ctas = 2) and for the FP16-accumulate kind; and the
+    library's own choice (tile_n = 0) for a row-sharded-rank shape (1024 x 8192: 224 wide) too."""
+    M, N, K = 1024, 8192 if fmt == "bf16" else 2048, 256
+    if fmt == "f16acc":
+        A, B, _ = _problem(M, N, K, "f16", seed=23)
+        C = tcxgen.normal_matrix((M, N), "f16", 23, tcxgen.STREAM_C, DEV)
+        run = lambda **kw: tcx.gemm(A, B, C, f16_acc=True, **kw)
+    else:
+        A, B, C = _problem(M, N, K, fmt, seed=23)
+        run = lambda **kw: tcx.gemm(A, B, C, **kw)
+    ref = run(tile_n=256, pairs=(1, 1))
+    outs = [run(tile_n=w) for w in (224, 192, 160, 128)] + [run(tile_n=224, max_ctas=2), run()]
+    torch.cuda.synchronize()
+    r = ref.view(torch.int16 if fmt == "f16acc" else torch.int32)
+    for o in outs:
+        assert torch.equal(o.view(r.dtype), r)
+
+
 @pytest.mark.parametrize("cg", [1, 2])
 def test_gemm_persistent_many_tiles_per_cta(cg):
     """few CTAs, many tiles each: exercises the smem ring and TMEM double-buffer phases."""

@@ -18,7 +18,10 @@ import bench  # noqa: E402
 def parse(v):
     kw = {}
     for part in v.split(","):
-        if part:
+        if part.startswith("env:"):          # env:NAME=VALUE (library A/B knobs read per call)
+            k, x = part[4:].split("=")
+            os.environ[k] = x
+        elif part:
             k, x = part.split("=")
             kw[k] = tuple(int(t) for t in x.split("x")) if "x" in x else int(x)
     return kw
