@@ -531,7 +531,12 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     // ring and no load will refill it, so the epilogue stages the whole tile there (warp e: CH
     // chunks of 4 KiB) — all C chunks are loaded at once and no chunk waits for an earlier store to
     // free its buffer.  The exposed tail of every launch (and all of a one-tile problem) shrinks.
-    constexpr bool RING_LAST = NH == 1 && P == 1 && EPI_WARPS * CH * 4096 <= C_::SMEM_DATA;
+    // (multicast groups too: the pairs of a group run the same cluster tiles, so by the time this
+    // pair's last accumulator is full no peer has a load left to land in this CTA's ring)
+#ifndef TCX_RING_LAST_MC
+#define TCX_RING_LAST_MC 1
+#endif
+    constexpr bool RING_LAST = NH == 1 && (P == 1 || TCX_RING_LAST_MC) && EPI_WARPS * CH * 4096 <= C_::SMEM_DATA;
     const int64_t q_last0 = (my_tiles - 1) * CH;             // first chunk of the last tile
     // origins of the (at most two) tiles the epilogue addresses at a time — this one and the next —
     // cached, so the raster's 64-bit divisions (~800 cycles) run once per tile, not once per chunk

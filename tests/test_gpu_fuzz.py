@@ -1,6 +1,6 @@
 """Seeded random-configuration fuzz of the GEMM front end and kernels: random shapes (ragged, tiny,
-multi-tile), kinds and kernel options (CTA mode, wide tiles, multicast groups, raster, persistent-grid
-caps, in-place D).  Two checks per sampled output:
+multi-tile), kinds and kernel options (CTA mode, wide and narrow tiles, multicast groups, raster,
+persistent-grid caps, in-place D).  Two checks per sampled output:
   * PARITY against the exact oracle (oracle.gemm_samples): INT8 bit-exact (wrapped), FP within the
     north_star bound (K+2) 2^-23 (sum|ab| + |c|);
   * CROSS-VALIDATION against the instruction model DESIGN.md §7 observed on B200 (fitted to the
@@ -34,6 +34,8 @@ def _dense_case(rng, i):
         opts["tile_n"] = 512
     elif r < 0.5:
         opts["pairs"] = [(1, 2), (2, 1), (2, 2)][int(rng.integers(3))]
+    elif r < 0.65:
+        opts["tile_n"] = int(rng.choice([224, 192, 160, 128]))      # narrow (wave-aware) pair tiles
     if rng.random() < 0.3:
         opts["group_m"] = int(rng.choice([-8, -2, 1, 3, 16]))
     if rng.random() < 0.3:
