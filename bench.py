@@ -382,6 +382,28 @@ def time_steps(work, steps, warmup, dist_on, sampler=None):
     return e0.elapsed_time(e1) / steps, launches, t0, t1
 
 
+def e2e_copy_bound(work, reps=5):
+    """the e2e step's floor on this box: the same H2D of every input and D2H of the result, both
+    directions at once on the e2e streams, with no GEMM (PCIe Gen5 x16 full duplex)"""
+    cur = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(cur)
+    for _ in range(reps):
+        work.s_in.wait_stream(cur)
+        work.s_out.wait_stream(cur)
+        with torch.cuda.stream(work.s_in):
+            for dst, src in zip(work.slots[0], work.h_ins):
+                dst.copy_(src, non_blocking=True)
+        with torch.cuda.stream(work.s_out):
+            work.hD.copy_(work.slots[1][-1], non_blocking=True)
+        cur.wait_stream(work.s_in)
+        cur.wait_stream(work.s_out)
+    e1.record(cur)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 def time_e2e(work, steps, warmup):
     """end-to-end through the public API: every step's H2D of its inputs (pinned host memory), the
     call, and the D2H of its result, pipelined over three streams; CUDA events from the first H2D
@@ -980,6 +1002,9 @@ def main():
             torch.distributed.all_reduce(io, op=torch.distributed.ReduceOp.SUM)
         e2e = {"value": round(ev, 3), "unit": work.unit, "h2d_bytes_per_step": int(io[0].item()),
                "d2h_bytes_per_step": int(io[1].item()), "ms_per_step": round(e2e_ms, 4)}
+        cb_ms = e2e_copy_bound(work)
+        e2e["copy_bound"] = {"ms_per_step": round(cb_ms, 4), "frac": round(cb_ms / e2e_ms, 4),
+                             "what": "the step's H2D + D2H alone, both directions at once, no GEMM (this rank)"}
 
     line = {"metric": metric, "value": round(value, 3), "unit": work.unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
