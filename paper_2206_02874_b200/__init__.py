@@ -186,6 +186,47 @@ def _rows_ok(name, t, shape, dtype):
         _need(t.is_contiguous(), f"{name}: must be contiguous")
 
 
+def _mat(name, t, rows, cols, dtype):
+    """the per-call check of a 2-D operand (shape, dtype, unit inner stride), cheap on the accepting
+    path (a GEMM call's host cost is part of every small call's latency); returns the row stride.
+    Any mismatch is re-checked by _rows_ok, which raises the precise error."""
+    sh = t.shape
+    if len(sh) != 2 or sh[0] != rows or sh[1] != cols or t.dtype != dtype:
+        _rows_ok(name, t, (rows, cols), dtype)
+    st = t.stride()
+    if st[1] != 1 and rows and cols:
+        _rows_ok(name, t, (rows, cols), dtype)
+    return st[0]
+
+
+def _tile3(name, t, count, m, n, dtype):
+    """the per-call check of a contiguous (count, m, n) tile array; mismatches re-checked by _rows_ok"""
+    sh = t.shape
+    if len(sh) != 3 or sh[0] != count or sh[1] != m or sh[2] != n or t.dtype != dtype or not t.is_contiguous():
+        _rows_ok(name, t, (count, m, n), dtype)
+
+
+def _device_of(*ts):
+    """the one CUDA device index all given tensors live on (None entries skipped); raises otherwise"""
+    d = -2
+    for t in ts:
+        if t is not None:
+            g = t.get_device()
+            if g < 0:
+                raise ValueError("tcx operates on CUDA tensors only (no CPU fallback)")
+            if d != g:
+                if d != -2:
+                    raise ValueError("tcx: all tensors of a call must be on one CUDA device")
+                d = g
+    return d
+
+
+def _stream_of(dev_index):
+    if _raw_stream is not None:
+        return _raw_stream(dev_index)
+    return torch.cuda.current_stream(dev_index).cuda_stream
+
+
 # ---------------------------------------------------------------------------------------- tiles
 def mma_tiles(A, B, C=None, D=None, tf32=False, tc05=False, f16_acc=False):
     """D_t = A_t B_t + C_t for A (count, 16, k), B (count, 8, k), C/D (count, 16, 8).
@@ -197,17 +238,20 @@ def mma_tiles(A, B, C=None, D=None, tf32=False, tc05=False, f16_acc=False):
     cd = S32 if ab == S8 else (F16 if f16_acc else F32)
     if C is not None and cd == F16 and C.dtype != torch.float16:
         raise ValueError("f16_acc: C must be float16")
-    _rows_ok("A", A, (count, m, k), A.dtype)
-    _rows_ok("B", B, (count, n, k), A.dtype)
+    _tile3("A", A, count, m, k, A.dtype)
+    _tile3("B", B, count, n, k, A.dtype)
     if C is not None:
-        _rows_ok("C", C, (count, m, n), _CD_TORCH[cd])
+        _tile3("C", C, count, m, n, _CD_TORCH[cd])
     if D is not None:
-        _rows_ok("D", D, (count, m, n), _CD_TORCH[cd])
-    _dev_check(A, B, C, D)
+        _tile3("D", D, count, m, n, _CD_TORCH[cd])
+    dev = _device_of(A, B, C, D)
     if D is None:
         D = torch.empty((count, m, n), dtype=_CD_TORCH[cd], device=A.device)
-    fn = lib().tcx_mma_tiles_tc05 if tc05 else lib().tcx_mma_tiles
-    _check(fn(ab, cd, m, n, k, count, _ptr(A), _ptr(B), _ptr(C), _ptr(D), _stream(A)))
+    L = _lib or lib()
+    fn = L.tcx_mma_tiles_tc05 if tc05 else L.tcx_mma_tiles
+    st = fn(ab, cd, m, n, k, count, A.data_ptr(), B.data_ptr(), _ptr(C), D.data_ptr(), _stream_of(dev))
+    if st:
+        _check(st)
     return D
 
 
@@ -242,23 +286,24 @@ def gemm(A, B, C=None, D=None, tf32=False, cta_group=0, max_ctas=0, group_m=0, t
     cd = S32 if ab == S8 else (F16 if f16_acc else F32)
     if cd == F16 and C is not None and C.dtype != torch.float16:
         raise ValueError("f16_acc: C must be float16")
-    _rows_ok("A", A, (M, K), A.dtype)
-    _rows_ok("B", B, (N, K), A.dtype)
-    if C is not None:
-        _rows_ok("C", C, (M, N), _CD_TORCH[cd])
-    if D is not None:
-        _rows_ok("D", D, (M, N), _CD_TORCH[cd])
-    _dev_check(A, B, C, D)
+    cdt = _CD_TORCH[cd]
+    lda = _mat("A", A, M, K, A.dtype)
+    ldb = _mat("B", B, N, K, A.dtype)
+    ldc = _mat("C", C, M, N, cdt) if C is not None else N
+    ldd = _mat("D", D, M, N, cdt) if D is not None else N
+    dev = _device_of(A, B, C, D)
     if D is None:
-        D = torch.empty((M, N), dtype=_CD_TORCH[cd], device=A.device)
-    ldc = C.stride(0) if C is not None else N
+        D = torch.empty((M, N), dtype=cdt, device=A.device)
+    L = _lib or lib()
     if not (cta_group or max_ctas or group_m or tile_n or pairs[0] or pairs[1] or _fault):
-        _check(lib().tcx_gemm(ab, cd, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(C), ldc, _ptr(D),
-                              D.stride(0), _stream(A)))
-        return D
-    opts = GemmOpts(cta_group, max_ctas, group_m, tile_n, pairs[0], pairs[1], (ctypes.c_int * 2)(_fault, 0))
-    _check(lib().tcx_gemm_ex(ab, cd, M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
-                             _ptr(C), ldc, _ptr(D), D.stride(0), ctypes.byref(opts), _stream(A)))
+        st = L.tcx_gemm(ab, cd, M, N, K, A.data_ptr(), lda, B.data_ptr(), ldb, _ptr(C), ldc, D.data_ptr(), ldd,
+                        _stream_of(dev))
+    else:
+        opts = GemmOpts(cta_group, max_ctas, group_m, tile_n, pairs[0], pairs[1], (ctypes.c_int * 2)(_fault, 0))
+        st = L.tcx_gemm_ex(ab, cd, M, N, K, A.data_ptr(), lda, B.data_ptr(), ldb, _ptr(C), ldc, D.data_ptr(), ldd,
+                           ctypes.byref(opts), _stream_of(dev))
+    if st:
+        _check(st)
     return D
 
 
@@ -328,17 +373,18 @@ def gemm_sp24(vals, meta_hw, B, C=None, D=None, cta_group=0, max_ctas=0, group_m
           "tensor from sp24_pack_meta")
     _need(meta_hw.numel() == sp24_meta_hw_bytes(M, K, ab),
           f"gemm_sp24: meta_hw has {meta_hw.numel()} bytes, ({M}, {K}) needs {sp24_meta_hw_bytes(M, K, ab)}")
-    if C is not None:
-        _rows_ok("C", C, (M, N), _CD_TORCH[cd])
-    if D is not None:
-        _rows_ok("D", D, (M, N), _CD_TORCH[cd])
-    _dev_check(vals, meta_hw, B, C, D)
+    cdt = _CD_TORCH[cd]
+    ldc = _mat("C", C, M, N, cdt) if C is not None else N
+    ldd = _mat("D", D, M, N, cdt) if D is not None else N
+    dev = _device_of(vals, meta_hw, B, C, D)
     if D is None:
-        D = torch.empty((M, N), dtype=_CD_TORCH[cd], device=vals.device)
+        D = torch.empty((M, N), dtype=cdt, device=vals.device)
     opts = GemmOpts(cta_group, max_ctas, group_m, int(tile_m), pairs[0], pairs[1], (ctypes.c_int * 2)(_knobs, 0))
-    _check(lib().tcx_gemm_sp24_ex(ab, cd, M, N, K, _ptr(vals), vals.stride(0), _ptr(meta_hw), _ptr(B), B.stride(0),
-                                  _ptr(C), C.stride(0) if C is not None else N, _ptr(D), D.stride(0),
-                                  ctypes.byref(opts), _stream(vals)))
+    st = (_lib or lib()).tcx_gemm_sp24_ex(ab, cd, M, N, K, vals.data_ptr(), vals.stride(0), meta_hw.data_ptr(),
+                                          B.data_ptr(), B.stride(0), _ptr(C), ldc, D.data_ptr(), ldd,
+                                          ctypes.byref(opts), _stream_of(dev))
+    if st:
+        _check(st)
     return D
 
 

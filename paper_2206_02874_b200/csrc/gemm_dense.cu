@@ -662,6 +662,7 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           sts128(pa, o);
         }
         TCX_STAMP(it, ch, 3);
+        if (ring) continue;                       // the last tile's stores leave together, below
         fence_proxy_async_smem();
         __syncwarp();
         TCX_STAMP(it, ch, 4);
@@ -675,7 +676,20 @@ gemm_dense_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
             bulk_wait_read<C_::NBE - C_::C_AHEAD>();
         }
         TCX_STAMP(it, ch, 6);
-        if (!ring) load_c(q + C_::C_AHEAD);
+        load_c(q + C_::C_AHEAD);
+      }
+      if (ring) {
+        // every chunk of the last tile has its own ring buffer: one proxy fence, then the CH TMA
+        // stores back to back (no per-chunk fence / store-issue round trip on the exposed tail)
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && !k_noepi) {
+          for (int ch = 0; ch < CH; ++ch) {
+            int x, y; coords(it * CH + ch, x, y);
+            tma_store_2d<HINT_D>(&tmD, ring_stg + ch * 4096, x, y, l2_evict_first());
+          }
+          bulk_commit();
+        }
       }
 #if TCX_WATCHDOG
       if (trace && e == 0 && lane == 0 && rank == 0) {
