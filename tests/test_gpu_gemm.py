@@ -137,6 +137,21 @@ def test_gemm_narrow_equals_default_and_persistent(fmt):
         assert torch.equal(o.view(r.dtype), r)
 
 
+def test_gemm_same_base_pointer_new_shape():
+    """the C ABI caches tensor-map descriptors keyed on every argument: views sharing a base pointer
+    with other rows / columns / strides must not reuse a stale descriptor (each result vs the oracle)"""
+    A, B, C = _problem(512, 512, 128, "bf16", seed=41)
+    for M, N in [(512, 512), (256, 512), (512, 256), (256, 128), (512, 512)]:
+        D = tcx.gemm(A[:M], B[:N], C[:M, :N].contiguous())
+        torch.cuda.synchronize()
+        _full_check("bf16", A[:M], B[:N], C[:M, :N].contiguous(), D)
+    Ap = torch.zeros(512, 192, dtype=torch.bfloat16, device=DEV)
+    Ap[:, :128] = A                                   # same data, padded rows (row stride 192)
+    D = tcx.gemm(Ap[:, :128], B, C)
+    torch.cuda.synchronize()
+    _full_check("bf16", A, B, C, D)
+
+
 @pytest.mark.parametrize("cg", [1, 2])
 def test_gemm_persistent_many_tiles_per_cta(cg):
     """few CTAs, many tiles each: exercises the smem ring and TMEM double-buffer phases."""
