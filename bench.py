@@ -991,7 +991,7 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        e2e_ms = time_e2e(work, max(3, min(args.steps, 10)), 2)
+        e2e_ms = time_e2e(work, max(3, min(args.steps, 50)), 2)
         if dist_on:
             t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
