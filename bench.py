@@ -130,6 +130,18 @@ class ClockSampler:
                 "power_w_median": round(statistics.median(pw), 1) if pw else None}
 
 
+def sparse_mwide(M, N, K, tf32=False, sm_count=148):
+    """the sparse tile height the library picks by default (gemm_sp24.cu launch_sp_kind): the 512 x 240
+    M-wide tile when M % 512 == 0, the K loop is long (K >= 16384, TF32 K >= 8192) and its tiles fill
+    the waves within 3% of the 256-row tiles' fill"""
+    pairs = sm_count // 2
+    nt = (N + 239) // 240
+
+    def fill(t):
+        return t / (((t + pairs - 1) // pairs) * pairs)
+    return M % 512 == 0 and K * (2 if tf32 else 1) >= 16384 and fill((M // 512) * nt) >= 0.97 * fill(((M + 255) // 256) * nt)
+
+
 def dense_kernel_name(kind, M, N, sm_count=148):
     """the dense kernel instance the library picks by default (gemm_dense.cu auto_pairs_1x2): 1 x 2
     multicast groups once there are >= 2 waves of 256 x 256 pair tiles over >= 2 tile columns"""
@@ -216,7 +228,7 @@ class Work:
             # (kept-product) rate is half of it and is reported beside it (DESIGN.md R-C13)
             self.flops = 2.0 * (m1 - m0) * N * K
             self.alg_bytes = self.vals.numel() * 2 + self.meta_hw.numel() + self.B.numel() * 2 + 8 * (m1 - m0) * N
-            mw = (m1 - m0) % 512 == 0 and (m1 - m0) * N * K >= 2 ** 43      # gemm_sp24.cu's M-wide default
+            mw = sparse_mwide(m1 - m0, N, K)                               # gemm_sp24.cu's M-wide default
             self.kernel = "gemm_sp24_kernel<2,f16,M-wide 512x240>" if mw else "gemm_sp24_kernel<2,f16,256x240>"
             self.step = lambda: tcx.gemm_sp24(self.vals, self.meta_hw, self.B, self.C, self.D)
             self.unit, self.bound = "TFLOP/s", "tensor"
@@ -243,7 +255,9 @@ class Work:
             self.flops = 2.0 * (m1 - m0) * N * K          # dense-equivalent (DESIGN.md R-C13)
             self.alg_bytes = (self.vals.numel() * esize + self.meta_hw.numel() + self.B.numel() * esize
                               + 8 * (m1 - m0) * N)
-            self.kernel = "gemm_sp24_kernel<2,%s>" % ("i8" if cfg == "c4sp" else "tf32")
+            self.kernel = ("gemm_sp24_kernel<2,i8>" if cfg == "c4sp" else
+                           "gemm_sp24_kernel<2,tf32,M-wide 512x240>" if sparse_mwide(m1 - m0, N, K, True)
+                           else "gemm_sp24_kernel<2,tf32,256x240>")
             tf = cfg == "c3sptf32"
             self.step = lambda: tcx.gemm_sp24(self.vals, self.meta_hw, self.B, self.C, self.D, tf32=tf)
             self.unit, self.bound = ("TOPS" if cfg == "c4sp" else "TFLOP/s"), "tensor"

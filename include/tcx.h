@@ -118,8 +118,9 @@ typedef struct {
                       instead of 128 tiles in 2).  Every width runs the same per-element MMA
                       sequence: D is bit-identical.  tcx_gemm_sp24 (the tile HEIGHT): 512 = the
                       512 x 240 pair tile (two M-halves share B; F16/BF16/TF32, M % 512 == 0 — the
-                      default there when M*N*K >= 2^43, i.e. calls long enough to run at the
-                      power cap), 256 = the 256 x 240 tile (the default otherwise) */
+                      default there when each tile's K loop is long, K >= 16384 (TF32: K >= 8192),
+                      and its tiles fill the SMs' waves within 3% of the 256-row tiles' fill),
+                      256 = the 256 x 240 tile (the default otherwise) */
   int pairs_m;     /* CTA pair only (not with tile_n = 512): groups of pairs_m x pairs_n CTA pairs   */
   int pairs_n;     /* compute adjacent pair tiles and are launched as preferred clusters; where the  */
                    /* hardware forms the cluster, A (sA) is TMA-multicast across the pairs_n pairs  */

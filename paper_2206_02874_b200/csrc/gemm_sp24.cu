@@ -568,15 +568,22 @@ tcx_status launch_sp(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
 template <int KIND>
 tcx_status launch_sp_kind(const GemmArgs& a, const DevInfo& dev, cudaStream_t s) {
   if (a.cta_group == 1) return launch_sp<1, KIND>(a, dev, s);
-  // tile_m = 512 (opts.tile_n field reused as the sparse tile height): the M-wide pair tile
-  // the 512 x 240 M-wide tile is the default for long calls (F16/BF16/TF32, M % 512 == 0, no
-  // multicast group, M*N*K >= 2^43 — a call of >= ~10 ms, which runs at the board's power cap): there
-  // its 31% fewer operand bytes per FLOP are worth more than its single-buffer drain (C5 +5.3%); on
-  // shorter calls the clock is not yet power-capped and the double-buffered 256 x 240 tile wins by
-  // 10-25% (profiles/r01_wide_tile_study.txt).  tile_n = 256 / 512 forces either.
+  // tile_m = 512 (opts.tile_n field reused as the sparse tile height): the 512 x 240 M-wide pair
+  // tile (F16/BF16/TF32, M % 512 == 0, no multicast group) is the default when each tile's K loop
+  // is long — K >= 16384 for F16/BF16, K >= 8192 for TF32 (half the MMA rate) — so its
+  // single-buffer drain is a small share of the tile, and when its tiles fill the SMs' waves about
+  // as well as the 256-row tiles do: its 31% fewer operand bytes per FLOP then win at the power cap
+  // (burst A/B over 8 shapes, profiles/r02_studies/sparse_tile_height/: K = 16384 F16 +3-4% incl.
+  // C5, TF32 8192^3 +3.2%, 16384^3 +13%; K = 8192 F16 the 256-row tile +5-8%).  tile_n = 256 /
+  // 512 forces either.
   if constexpr (KIND != KIND_I8) {
     const bool grouped = a.pairs_m > 1 || a.pairs_n > 1;
-    const bool long_call = (double)a.M * (double)a.N * (double)a.K >= 8796093022208.0;   // 2^43
+    const int64_t k_time = a.K * (KIND == KIND_TF32 ? 2 : 1);      // the K loop in F16-MMA units
+    int64_t pairs = dev.sm_count / 2;
+    if (a.max_ctas > 0 && a.max_ctas / 2 < pairs) pairs = a.max_ctas / 2 > 0 ? a.max_ctas / 2 : 1;
+    const int64_t nt = (a.N + 239) / 240;
+    auto fill = [&](int64_t tiles) { return (double)tiles / (double)(((tiles + pairs - 1) / pairs) * pairs); };
+    const bool long_call = k_time >= 16384 && fill((a.M / 512) * nt) >= 0.97 * fill(((a.M + 255) / 256) * nt);
     if (a.M % 512 == 0 && (a.tile_n == 512 || (a.tile_n == 0 && !grouped && long_call))) {
       // M-wide tile, optionally in multicast groups of pairs: pairs_m pairs of a column share B
       // (1024 x 240 per group), pairs_n pairs of a row share sA and metadata rows (512 x 480)
