@@ -142,12 +142,35 @@ def sparse_mwide(M, N, K, tf32=False, sm_count=148):
     return M % 512 == 0 and K * (2 if tf32 else 1) >= 16384 and fill((M // 512) * nt) >= 0.97 * fill(((M + 255) // 256) * nt)
 
 
-def dense_kernel_name(kind, M, N, sm_count=148):
-    """the dense kernel instance the library picks by default (gemm_dense.cu auto_pairs_1x2): 1 x 2
-    multicast groups once there are >= 2 waves of 256 x 256 pair tiles over >= 2 tile columns"""
-    m_tiles, n_tiles = (M + 255) // 256, (N + 255) // 256
-    groups = n_tiles >= 2 and m_tiles * n_tiles >= 2 * (sm_count // 2)
-    return f"gemm_dense_kernel<2,{kind},1,1,{2 if groups else 1}>" + (" (1x2 groups)" if groups else "")
+def dense_kernel_name(kind, M, N, K=8192, sm_count=148):
+    """the dense kernel instance the library picks by default (gemm_dense.cu): the wave-aware narrow
+    width when 256-wide tiles fill the waves poorly, the 256 x 512 tile for long K loops (K_eff >=
+    16384 with a wave fill within 3%), else 1 x 2 multicast groups once there are >= 2 waves of
+    256 x 256 pair tiles over >= 2 tile columns"""
+    pairs = sm_count // 2
+    mt = (M + 255) // 256
+
+    def waves_cost(w, rate):
+        t = mt * ((N + w - 1) // w)
+        return ((t + pairs - 1) // pairs) * w * 1000 // rate
+
+    c256 = waves_cost(256, 1000)
+    best, bc = 256, c256
+    for w, rate in ((224, 979), (192, 944), (160, 879), (128, 806)):
+        c = waves_cost(w, rate)
+        if c < bc and 20 * c <= 19 * c256:
+            best, bc = w, c
+    if best != 256:
+        return f"gemm_dense_kernel<2,{kind},1,1,1,{best}> (256x{best} tile)"
+
+    def fill(t):
+        return t / (((t + pairs - 1) // pairs) * pairs)
+    k_eff = 2 * K if kind == 1 else K // 2 if kind == 2 else K
+    if kind != "f16acc" and k_eff >= 16384 and fill(mt * ((N + 511) // 512)) >= 0.97 * fill(mt * ((N + 255) // 256)):
+        return f"gemm_dense_kernel<2,{kind},2,1,1,256> (256x512 tile)"
+    n_tiles = (N + 255) // 256
+    groups = n_tiles >= 2 and mt * n_tiles >= 2 * pairs
+    return f"gemm_dense_kernel<2,{kind},1,1,{2 if groups else 1},256>" + (" (1x2 groups)" if groups else "")
 
 
 # ----------------------------------------------------------------------------------- workloads
@@ -179,7 +202,7 @@ class Work:
             self.flops = 2.0 * (m1 - m0) * N * K
             self.alg_bytes = self.A.numel() * self.A.element_size() + self.B.numel() * self.B.element_size() + 8 * (m1 - m0) * N
             self.tf32 = fmt == "tf32"
-            self.kernel = dense_kernel_name(0 if fmt == "bf16" else 1, m1 - m0, N)
+            self.kernel = dense_kernel_name(0 if fmt == "bf16" else 1, m1 - m0, N, K)
             self.step = lambda: tcx.gemm(self.A, self.B, self.C, self.D, tf32=self.tf32)
             self.unit, self.bound = "TFLOP/s", "tensor"
         elif cfg == "c3f16acc":              # NEXT-2: FP16 inputs, FP16 accumulator, FP16 C/D at C3's shape
@@ -193,7 +216,7 @@ class Work:
             self.D = torch.empty(m1 - m0, N, dtype=torch.float16, device=dev)
             self.flops = 2.0 * (m1 - m0) * N * K
             self.alg_bytes = 2 * (self.A.numel() + self.B.numel()) + 4 * (m1 - m0) * N
-            self.kernel = dense_kernel_name("f16acc", m1 - m0, N)
+            self.kernel = dense_kernel_name("f16acc", m1 - m0, N, K)
             self.step = lambda: tcx.gemm(self.A, self.B, self.C, self.D, f16_acc=True)
             self.unit, self.bound = "TFLOP/s", "tensor"
         elif cfg == "c4":
@@ -207,7 +230,7 @@ class Work:
             self.D = torch.empty(m1 - m0, N, dtype=torch.int32, device=dev)
             self.flops = 2.0 * (m1 - m0) * N * K
             self.alg_bytes = self.A.numel() + self.B.numel() + 8 * (m1 - m0) * N
-            self.kernel = dense_kernel_name(2, m1 - m0, N)
+            self.kernel = dense_kernel_name(2, m1 - m0, N, K)
             self.step = lambda: tcx.gemm(self.A, self.B, self.C, self.D)
             self.unit, self.bound = "TOPS", "tensor"
         elif cfg in ("c5", "c5s"):       # c5s: an 8192-row slice of C5 (profiling only)

@@ -115,8 +115,9 @@ typedef struct {
                       narrower width itself when the 256-wide tiles fill their last wave on the
                       SMs poorly and the narrower one is >= 5% cheaper in (waves x width) — e.g.
                       1024 x 8192 (C3 row-sharded over 8 GPUs): 224 (148 tiles = 2 full waves
-                      instead of 128 tiles in 2).  Every width runs the same per-element MMA
-                      sequence: D is bit-identical.  tcx_gemm_sp24 (the tile HEIGHT): 512 = the
+                      instead of 128 tiles in 2); and 512 when the K loop is long (K >= 16384
+                      BF16/FP16, 8192 TF32, 32768 INT8) and its tiles fill the waves as well.
+                      Every width runs the same per-element MMA sequence: D is bit-identical.  tcx_gemm_sp24 (the tile HEIGHT): 512 = the
                       512 x 240 pair tile (two M-halves share B; F16/BF16/TF32, M % 512 == 0 — the
                       default there when each tile's K loop is long, K >= 16384 (TF32: K >= 8192),
                       and its tiles fill the SMs' waves within 3% of the 256-row tiles' fill),

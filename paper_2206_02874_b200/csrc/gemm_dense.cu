@@ -777,8 +777,8 @@ tcx_status launch_t(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUten
   cfg.gridDim = dim3((unsigned)(clusters * CL));
 #if TCX_WATCHDOG
   if (getenv("TCX_DEBUG_LAUNCH"))   // debug library: print the launch shape
-    fprintf(stderr, "tcx_gemm: grid %u CTAs, cluster %d (pairs %dx%d), %lld cluster tiles\n", cfg.gridDim.x, CL, PM, PN,
-            (long long)(((m_tiles + PM - 1) / PM) * ((n_tiles + PN - 1) / PN)));
+    fprintf(stderr, "tcx_gemm: grid %u CTAs, cluster %d (pairs %dx%d), tile %dx%d, %lld cluster tiles\n", cfg.gridDim.x, CL,
+            PM, PN, C_::TILE_M, C_::TILE_N, (long long)(((m_tiles + PM - 1) / PM) * ((n_tiles + PN - 1) / PN)));
 #endif
   const uint32_t idesc = make_idesc(KIND, a_fmt, BM * CG, C_::BN);
   TCX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tA, tB, tC, tD, (int64_t)a.M, (int64_t)a.N, (int64_t)a.K,
@@ -855,11 +855,31 @@ tcx_status launch_narrow(int w, const GemmArgs& a, const DevInfo& dev, cudaStrea
   }
 }
 
+// Long K loops (library choice): the 256 x 512 pair tile moves 25% fewer operand bytes per FLOP but
+// its single accumulator exposes a drain of fixed length per tile, so it wins once a tile's K loop
+// is long enough for the drain to be a small share — K >= 16384 BF16/FP16 MMA-equivalents (TF32
+// runs at half the rate: K >= 8192; INT8 at twice: K >= 32768) — and when its tiles fill the waves
+// within 3% of the 256-wide tiles' fill.  Burst A/B (profiles/r02_studies/dense_wide_long_k/):
+// BF16 16384^3 +4.3%, 8192 x 8192 x 32768 +4.0%, 8192 x 8192 x 16384 +1.1%; TF32 16384^3 +8.0%,
+// 8192^3 +0.5%; INT8 16384 x 16384 x 32768 +6.8%; at K_eff = 8192 (C3 BF16, C4) the default wins.
+template <int KIND>
+static bool auto_wide(const GemmArgs& a, const DevInfo& dev) {
+  if (a.tile_n != 0 || !a.pairs_auto || a.cta_group != 2 || KIND == KIND_F16ACC) return false;
+  const int64_t k_eff = KIND == KIND_TF32 ? 2 * a.K : KIND == KIND_I8 ? a.K / 2 : a.K;
+  if (k_eff < 16384) return false;
+  int64_t pairs = dev.sm_count / 2;
+  if (a.max_ctas > 0 && a.max_ctas / 2 < pairs) pairs = a.max_ctas / 2 > 0 ? a.max_ctas / 2 : 1;
+  const int64_t mt = (a.M + 255) / 256;
+  auto fill = [&](int64_t t) { return (double)t / (double)(((t + pairs - 1) / pairs) * pairs); };
+  return fill(mt * ((a.N + 511) / 512)) >= 0.97 * fill(mt * ((a.N + 255) / 256));
+}
+
 template <int KIND>
 tcx_status launch_kind(const GemmArgs& a, const DevInfo& dev, cudaStream_t s, CUtensorMapDataType dt, int a_fmt) {
   if (a.cta_group == 1) return launch_t<1, KIND, 1>(a, dev, s, dt, a_fmt);
   const int w = wave_tile_width(a, dev);
   if (w != 256) return launch_narrow<KIND>(w, a, dev, s, dt, a_fmt);
+  if (auto_wide<KIND>(a, dev)) return launch_t<2, KIND, 2>(a, dev, s, dt, a_fmt);
   if (auto_pairs_1x2(a, dev)) return launch_t<2, KIND, 1, 1, 2>(a, dev, s, dt, a_fmt);
   // 256 x 512 pair tiles only when asked: they cut L2->SM operand traffic by 25% (and run at a
   // higher clock under the power cap), but the single-buffered accumulator exposes the epilogue,

@@ -163,6 +163,40 @@ print("TILES", tiles_run(1024, 8192), tiles_run(1024, 8192, tile_n=256), tiles_r
         assert got[1] == 128 and got[0] >= 128, got
 
 
+def test_dense_default_tile_choices(tmp_path):
+    """the library's dense tile choices (gemm_dense.cu), read from the debug build's launch report:
+    C3 (BF16 8192^3) runs 256 x 256 tiles in 1 x 2 multicast groups; a long K loop (BF16 K = 16384,
+    TF32 K = 8192) the 256 x 512 tile; a row-sharded rank (1024 x 8192) the 256 x 224 tile."""
+    code = PROBLEM + """
+def run(fmt, M, N, K):
+    A = tcxgen.normal_matrix((M, K), fmt, 9, tcxgen.STREAM_A, dev)
+    B = tcxgen.normal_matrix((N, K), fmt, 9, tcxgen.STREAM_B, dev)
+    tcx.gemm(A, B, None, tf32=(fmt == "tf32"))
+    torch.cuda.synchronize()
+run("bf16", 8192, 8192, 8192)
+run("bf16", 8192, 8192, 16384)
+run("tf32", 8192, 8192, 8192)
+run("bf16", 1024, 8192, 8192)
+print("OK")
+"""
+    env_keep = os.environ.get("TCX_DEBUG_LAUNCH")
+    os.environ["TCX_DEBUG_LAUNCH"] = "1"
+    try:
+        r = _run(code, tmp_path)
+    finally:
+        if env_keep is None:
+            del os.environ["TCX_DEBUG_LAUNCH"]
+        else:
+            os.environ["TCX_DEBUG_LAUNCH"] = env_keep
+    assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-2000:]
+    lines = [ln for ln in r.stderr.splitlines() if ln.startswith("tcx_gemm:")]
+    assert len(lines) == 4, r.stderr[-2000:]
+    if torch.cuda.get_device_properties(0).multi_processor_count == 148:
+        assert "pairs 1x2), tile 256x256" in lines[0], lines[0]
+        assert "tile 256x512" in lines[1] and "tile 256x512" in lines[2], lines[1:3]
+        assert "tile 256x224" in lines[3], lines[3]
+
+
 def test_sparse_tile_trace(tmp_path):
     """tcx_debug_trace on the 2:4 kernel (narrow and M-wide tiles): every tile recorded, in order."""
     code = """
