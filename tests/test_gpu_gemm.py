@@ -137,6 +137,21 @@ def test_gemm_narrow_equals_default_and_persistent(fmt):
         assert torch.equal(o.view(r.dtype), r)
 
 
+@pytest.mark.parametrize("fmt,K", [("bf16", 16384), ("tf32", 8192), ("s8", 32768)])
+def test_gemm_long_k_default_wide_tile(fmt, K):
+    """long K loops take the 256 x 512 tile by default (K_eff >= 16384): with few pairs (max_ctas = 8)
+    each pair runs several wide tiles back to back through the half-0 lookahead; D equals the
+    256-wide tile's bit for bit, and sampled outputs match the oracle (bound / bit-exact INT8)."""
+    M, N = 1024, 2048
+    A, B, C = _problem(M, N, K, fmt, seed=K + 5)
+    Dd = tcx.gemm(A, B, C, tf32=(fmt == "tf32"), max_ctas=8)
+    Dn = tcx.gemm(A, B, C, tf32=(fmt == "tf32"), max_ctas=8, tile_n=256, pairs=(1, 1))
+    torch.cuda.synchronize()
+    assert torch.equal(Dd.view(torch.int32), Dn.view(torch.int32))
+    rows, cols = gemm_sample_coords(M, N, 256, 512, nsamp=4096)
+    check_gemm_samples(TORCH2ORACLE[A.dtype], A, B, C, Dd, rows, cols, K, f"long-K {fmt}")
+
+
 def test_gemm_same_base_pointer_new_shape():
     """the C ABI caches tensor-map descriptors keyed on every argument: views sharing a base pointer
     with other rows / columns / strides must not reuse a stale descriptor (each result vs the oracle)"""
