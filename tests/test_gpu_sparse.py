@@ -204,6 +204,26 @@ def test_sparse_m_wide_tile_vs_oracle_and_narrow(shape):
     fp_bound_check(host_bits(Dw).ravel(), ref, absv, K, f"sp24 mwide {shape}")
 
 
+def test_sparse_long_k_default_m_wide():
+    """a long K loop (K = 16384) takes the M-wide tile by default: with few pairs (max_ctas = 4) each
+    runs several 512 x 240 tiles; D equals the 256-row tile's bit for bit and matches the oracle on
+    samples (the library's choice itself is mirrored by bench.sparse_mwide, test_bench_kernel_choice)."""
+    M, N, K = 1024, 480, 16384
+    vals, meta, _ = _dense_24(M, K, 77)
+    B = tcxgen.normal_matrix((N, K), "f16", 78, tcxgen.STREAM_B, DEV)
+    C = tcxgen.normal_matrix((M, N), "f32", 79, tcxgen.STREAM_C, DEV)
+    hw = tcx.sp24_pack_meta(meta, M, K)
+    Dd = tcx.gemm_sp24(vals, hw, B, C, max_ctas=4)
+    Dn = tcx.gemm_sp24(vals, hw, B, C, tile_m=256, max_ctas=4)
+    torch.cuda.synchronize()
+    assert torch.equal(Dd.view(torch.int32), Dn.view(torch.int32))
+    rng = np.random.default_rng(5)
+    rows, cols = rng.integers(0, M, 2048), rng.integers(0, N, 2048)
+    ref, absv = O.gemm_samples(O.F16, O.sp24_expand(host_bits(vals), host_bits(meta), K), host_bits(B),
+                               host_bits(C), rows, cols)
+    fp_bound_check(host_bits(Dd)[rows, cols], ref, absv, K, "sp24 long-K default")
+
+
 def test_sparse_m_wide_integer_bit_exact_bf16():
     M, N, K = 1024, 480, 1024
     vals, meta, dense = _dense_24(M, K, 15, torch.bfloat16, integer=True)
