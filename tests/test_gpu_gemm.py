@@ -152,6 +152,20 @@ def test_gemm_long_k_default_wide_tile(fmt, K):
     check_gemm_samples(TORCH2ORACLE[A.dtype], A, B, C, Dd, rows, cols, K, f"long-K {fmt}")
 
 
+@pytest.mark.parametrize("fmt,K", [("bf16", 16384), ("tf32", 8192)])
+def test_gemm_long_k_wide_full_waves(fmt, K):
+    """>= 2 full waves of long-K wide tiles (the default there): bit-identical to the plain 256-wide
+    tile, oracle on samples incl. every tile corner."""
+    M, N = 4096, 8192
+    A, B, C = _problem(M, N, K, fmt, seed=K + 11)
+    Dd = tcx.gemm(A, B, C, tf32=(fmt == "tf32"))
+    Dn = tcx.gemm(A, B, C, tf32=(fmt == "tf32"), tile_n=256, pairs=(1, 1))
+    torch.cuda.synchronize()
+    assert torch.equal(Dd.view(torch.int32), Dn.view(torch.int32))
+    rows, cols = gemm_sample_coords(M, N, 256, 512, nsamp=8192)
+    check_gemm_samples(TORCH2ORACLE[A.dtype], A, B, C, Dd, rows, cols, K, f"long-K waves {fmt}")
+
+
 def test_gemm_same_base_pointer_new_shape():
     """the C ABI caches tensor-map descriptors keyed on every argument: views sharing a base pointer
     with other rows / columns / strides must not reuse a stale descriptor (each result vs the oracle)"""
