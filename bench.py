@@ -1006,6 +1006,7 @@ def main():
 
     work = Work(args.config, rank, world, dev, scaling=args.scaling)
     torch.cuda.synchronize()
+    time.sleep(1.0)                       # start from an idle board, as every "also" config does
     sampler = ClockSampler(local)
     sampler.start()
     ms, launches, t0, t1 = time_steps(work, args.steps, args.warmup, dist_on)
@@ -1083,6 +1084,11 @@ def main():
         for extra in ("c1", "c3tf32", "c3f16acc", "c4", "c3sptf32", "c4sp", "c5"):
             try:
                 w2 = Work(extra, 0, 1, dev)
+                # every config starts from the same idle board (as tools/ab_burst.py A/Bs do): the
+                # previous config's power-capped run and this one's input generation leave the clock
+                # in a history-dependent state for tens of ms
+                torch.cuda.synchronize()
+                time.sleep(1.0)
                 sampler.samples = []
                 sampler.start()
                 ms2, l2, u0, u1 = time_steps(w2, max(5, min(args.steps, 20)), 3, False)
