@@ -166,6 +166,20 @@ def test_gemm_long_k_wide_full_waves(fmt, K):
     check_gemm_samples(TORCH2ORACLE[A.dtype], A, B, C, Dd, rows, cols, K, f"long-K waves {fmt}")
 
 
+def test_gemm_tall_m_large_coordinates():
+    """maximum-size edge: ~2^20 rows (TMA row coordinates past 2^20, D > 2^33 bytes, far past any
+    32-bit byte offset), ragged M and N: sampled outputs incl. the last rows / columns vs the oracle."""
+    M, N, K = (1 << 20) + 200, 2048 + 8, 64
+    A, B, C = _problem(M, N, K, "bf16", seed=101, with_c=False)
+    D = tcx.gemm(A, B, None)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(3)
+    rows = np.concatenate([rng.integers(0, M, 4096), np.arange(M - 300, M)])
+    cols = np.concatenate([rng.integers(0, N, 4096), rng.integers(N - 40, N, 300)])
+    check_gemm_samples(TORCH2ORACLE[A.dtype], A, B, None, D, rows, cols, K, "tall M")
+    del A, B, D
+
+
 def test_gemm_same_base_pointer_new_shape():
     """the C ABI caches tensor-map descriptors keyed on every argument: views sharing a base pointer
     with other rows / columns / strides must not reuse a stale descriptor (each result vs the oracle)"""

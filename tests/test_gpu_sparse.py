@@ -224,6 +224,27 @@ def test_sparse_long_k_default_m_wide():
     fp_bound_check(host_bits(Dd)[rows, cols], ref, absv, K, "sp24 long-K default")
 
 
+@pytest.mark.parametrize("tile_m", [256, 512])
+def test_sparse_tall_m_large_coordinates(tile_m):
+    """maximum-size edge for the 2:4 kernel: 2^20 rows (metadata-atom and row coordinates far past
+    2^16, D of 1 GiB), both tile heights; sampled outputs incl. the last rows vs the oracle (only the
+    sampled rows are expanded on the host)."""
+    M, N, K = 1 << 20, 240 + 16, 256
+    vals, meta = tcxgen.sp24_problem(M, K, 91, "f16", DEV)
+    B = tcxgen.normal_matrix((N, K), "f16", 92, tcxgen.STREAM_B, DEV)
+    hw = tcx.sp24_pack_meta(meta, M, K)
+    D = tcx.gemm_sp24(vals, hw, B, None, tile_m=tile_m)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(tile_m)
+    urows = np.unique(np.concatenate([rng.integers(0, M, 512), np.arange(M - 64, M)]))
+    idx = torch.from_numpy(urows).to(DEV)
+    dense = O.sp24_expand(host_bits(vals[idx]), host_bits(meta[idx]), K)
+    rr = np.repeat(np.arange(len(urows)), 8)
+    cc = rng.integers(0, N, len(rr))
+    ref, absv = O.gemm_samples(O.F16, dense, host_bits(B), None, rr, cc)
+    fp_bound_check(host_bits(D)[urows[rr], cc], ref, absv, K, f"sp24 tall M tile_m={tile_m}")
+
+
 def test_sparse_m_wide_integer_bit_exact_bf16():
     M, N, K = 1024, 480, 1024
     vals, meta, dense = _dense_24(M, K, 15, torch.bfloat16, integer=True)
