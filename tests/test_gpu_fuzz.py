@@ -43,7 +43,7 @@ def _dense_case(rng, i):
     return fmt, M, N, K, opts, rng.random() < 0.2
 
 
-@pytest.mark.parametrize("i", range(32))
+@pytest.mark.parametrize("i", range(96))
 def test_dense_fuzz(i):
     rng = np.random.default_rng(1000 + i)
     fmt, M, N, K, opts, in_place = _dense_case(rng, i)
@@ -73,7 +73,7 @@ def test_dense_fuzz(i):
     assert np.array_equal(want, got), (fmt, M, N, K, opts, in_place, int((want != got).sum()))
 
 
-@pytest.mark.parametrize("i", range(12))
+@pytest.mark.parametrize("i", range(32))
 def test_sparse_fuzz(i):
     rng = np.random.default_rng(2000 + i)
     M = int(rng.integers(1, 6)) * 256
@@ -106,7 +106,7 @@ def test_sparse_fuzz(i):
     assert np.array_equal(want, got), (M, N, K, opts, int((want != got).sum()))
 
 
-@pytest.mark.parametrize("i", range(12))
+@pytest.mark.parametrize("i", range(24))
 def test_tiles_fuzz(i):
     """tcx_mma_tiles over random formats / k / counts, C present or not, FP32 or FP16 C/D: every
     output of every tile equals the instruction model (C as the MMA's C operand) bit for bit."""
