@@ -37,7 +37,9 @@ def main():
     for r in range(rounds):
         for v in (variants if r % 2 == 0 else variants[::-1]):
             kw = parse(v)
-            if sparse:
+            if cfg == "c1":                              # the tile batch has no kernel options
+                w.step = base
+            elif sparse:
                 w.step = lambda: w.tcx.gemm_sp24(w.vals, w.meta_hw, w.B, w.C, w.D, tf32=cfg == "c3sptf32", **kw)
             else:
                 w.step = lambda: w.tcx.gemm(w.A, w.B, w.C, w.D, tf32=getattr(w, "tf32", False),
