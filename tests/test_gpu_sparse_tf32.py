@@ -138,3 +138,30 @@ def test_tf32_sparse_multicast_bit_exact(pairs):
     ref = dense.double() @ B.double().T
     torch.cuda.synchronize()
     assert torch.equal(D.double(), ref)
+
+
+def test_tf32_1to2_c3_shape_full_size_default_tile():
+    """TF32 1:2 at C3's shape (8192^3, the bench's c3sptf32 operand): the library's default (the
+    512 x 240 M-wide tile since K_eff = 16384) bit-identical to the 256-row tile over the whole D, and
+    >= 65,536 sampled outputs (every 256-row tile's corner rows among them) within the bound of the
+    exact oracle."""
+    M = N = K = 8192
+    vals, meta = tcxgen.sp12_problem_tf32(M, K, 0, DEV)
+    B = tcxgen.normal_matrix((N, K), "tf32", 0, tcxgen.STREAM_B, DEV)
+    hw = tcx.sp24_pack_meta(meta, M, K, ab=tcx.TF32)
+    Dd = tcx.gemm_sp24(vals, hw, B, None, tf32=True)
+    Dn = tcx.gemm_sp24(vals, hw, B, None, tf32=True, tile_m=256)
+    torch.cuda.synchronize()
+    assert torch.equal(Dd.view(torch.int32), Dn.view(torch.int32))
+    del Dn
+    rng = np.random.default_rng(1)
+    corner = sorted({r for m0 in range(0, M, 256) for r in (m0, m0 + 255)})
+    rows = np.array(sorted(set(corner) | set(rng.integers(0, M, 2048 - len(corner)).tolist())))
+    idx = torch.from_numpy(rows).to(DEV)
+    dense_rows = O.sp24_expand(host_bits(vals[idx]), host_bits(meta[idx]), K)
+    ri = np.repeat(np.arange(len(rows)), -(-65536 // len(rows)))
+    ci = rng.integers(0, N, ri.size)
+    ref, absv = O.gemm_samples(O.TF32, dense_rows, host_bits(B), None, ri, ci)
+    got = host_bits(Dd[idx])[ri, ci]
+    assert ri.size >= 65536
+    fp_bound_check(got, ref, absv, K, "TF32 1:2 8192^3")
